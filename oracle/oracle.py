@@ -1,0 +1,289 @@
+"""TEST INFRASTRUCTURE ONLY -- CPU oracle for the Dykstra triangle sweep.
+
+Two restatements of the reference's hot path (arXiv 1901.10084 reference
+package ``metricproj``), used only by ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py`` (``cpu_baseline`` and ``--impl reference``) as the checker /
+CPU baseline.  The product (``paper_1901_10084_b200``) never imports this.
+
+* :class:`OracleSolver` drives ``libmetricproj_oracle.so`` (``metricproj_oracle.c``,
+  a C port of ``_kernels.py:28-220`` + ``solver.py:116-210``) and computes the
+  per-pass objectives with numpy exactly as ``core.py:275-339`` does.
+* :func:`py_pass` is a pure-Python loop restatement for tiny n, used to
+  cross-check the C port inside the CPU test suite.
+
+Parity is pinned: ``tests/golden/`` holds vectors produced by the unmodified
+reference (``tests/golden/make_golden.py``); ``tests/test_oracle.py`` checks
+both restatements against them bit for bit.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmetricproj_oracle.so")
+THETA_FLOOR = 1e-15  # _kernels.py:20
+KINDS = {"serial": 0, "diagonal": 1, "tiled": 2}
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle in place (``make -C oracle``)."""
+    src = os.path.join(HERE, "metricproj_oracle.c")
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        D = ctypes.POINTER(ctypes.c_double)
+        I = ctypes.POINTER(ctypes.c_int64)
+        L.mpo_create.restype = P
+        L.mpo_create.argtypes = [ctypes.c_int64, D, D, D, ctypes.c_double, ctypes.c_int,
+                                 ctypes.c_int64, ctypes.c_int]
+        L.mpo_destroy.argtypes = [P]
+        L.mpo_set_state.argtypes = [P, D, D]
+        L.mpo_get_state.argtypes = [P, D, D]
+        L.mpo_get_pair_duals.argtypes = [P, D]
+        L.mpo_dual_count.restype = ctypes.c_int64
+        L.mpo_dual_count.argtypes = [P]
+        L.mpo_get_duals.argtypes = [P, I, D]
+        L.mpo_run_pass.restype = ctypes.c_double
+        L.mpo_run_pass.argtypes = [P, I]
+        L.mpo_max_violation.restype = ctypes.c_double
+        L.mpo_max_violation.argtypes = [D, D, D, ctypes.c_int64]
+        L.mpo_num_rounds.restype = ctypes.c_int64
+        L.mpo_num_rounds.argtypes = [P]
+        L.mpo_num_tiles.restype = ctypes.c_int64
+        L.mpo_num_tiles.argtypes = [P]
+        L.mpo_get_schedule.argtypes = [P, I, I]
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+@dataclass
+class OracleStats:
+    """Mirror of core.PassStats (core.py:259-267)."""
+    pass_index: int
+    primal_objective: float
+    dual_objective: float
+    duality_gap: float
+    max_violation: float
+    steps: int
+
+
+def pair_count(n):
+    return n * (n - 1) // 2
+
+
+class OracleSolver:
+    """Reference-order CPU solver over packed arrays (core.py layout)."""
+
+    def __init__(self, n, d_flat, w_flat, eps, reg_x=None, reg_f=None,
+                 kind="tiled", b=40, workers=1):
+        m = pair_count(n)
+        self.n, self.m, self.eps = n, m, float(eps)
+        self.d_flat = np.ascontiguousarray(d_flat, dtype=np.float64)
+        self.w_flat = np.ascontiguousarray(w_flat, dtype=np.float64)
+        self.reg_x = np.ones(m) if reg_x is None else np.ascontiguousarray(reg_x, dtype=np.float64)
+        self.reg_f = np.ones(m) if reg_f is None else np.ascontiguousarray(reg_f, dtype=np.float64)
+        self.kind, self.b, self.workers = kind, b, workers
+        L = lib()
+        self._h = L.mpo_create(n, _dp(self.d_flat), _dp(self.reg_x), _dp(self.reg_f),
+                               self.eps, KINDS[kind], b, workers)
+        if not self._h:
+            raise ValueError("oracle rejected the configuration")
+        # Dykstra start (solver.py:108-113): x = 0, f = -w / (eps * reg_f)
+        x0 = np.zeros(m)
+        f0 = -self.w_flat / (self.eps * self.reg_f)
+        L.mpo_set_state(self._h, _dp(x0), _dp(f0))
+        self.passes = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mpo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def state(self):
+        x = np.empty(self.m)
+        f = np.empty(self.m)
+        lib().mpo_get_state(self._h, _dp(x), _dp(f))
+        return x, f
+
+    def set_state(self, x, f):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        lib().mpo_set_state(self._h, _dp(x), _dp(f))
+
+    def pair_duals(self):
+        pd = np.empty((self.m, 2))
+        lib().mpo_get_pair_duals(self._h, _dp(pd))
+        return pd
+
+    def duals(self):
+        c = lib().mpo_dual_count(self._h)
+        keys = np.empty(c, dtype=np.int64)
+        vals = np.empty(c)
+        if c:
+            lib().mpo_get_duals(self._h, _ip(keys), _dp(vals))
+        return keys, vals
+
+    def schedule(self):
+        L = lib()
+        nr = L.mpo_num_rounds(self._h)
+        nt = L.mpo_num_tiles(self._h)
+        rn = np.empty(nr, dtype=np.int64)
+        xz = np.empty((nt, 2), dtype=np.int64)
+        L.mpo_get_schedule(self._h, _ip(rn), _ip(xz))
+        return rn, xz
+
+    def run_pass(self):
+        steps = ctypes.c_int64(0)
+        viol = lib().mpo_run_pass(self._h, ctypes.byref(steps))
+        x, f = self.state()
+        pd = self.pair_duals()
+        primal, dual = objectives(self.eps, self.w_flat, self.d_flat, self.reg_x, self.reg_f, x, f, pd)
+        st = OracleStats(self.passes, primal, dual, primal - dual, viol, steps.value)
+        self.passes += 1
+        return st
+
+
+def objectives(eps, w_flat, d_flat, reg_x, reg_f, x, f, pd):
+    """primal_objective (core.py:275-282) and dual_objective_from_state
+    (core.py:330-339, with b_dot_y of core.py:314-317)."""
+    lin = float(np.dot(w_flat, f))
+    quad = float(np.dot(reg_x * x, x) + np.dot(reg_f * f, f))
+    primal = lin + 0.5 * eps * quad
+    bdy = float(np.dot(d_flat, pd[:, 0] - pd[:, 1]))
+    dual = -bdy - 0.5 * eps * quad
+    return primal, dual
+
+
+def max_violation(x, f, d_flat, n):
+    """Exact scan over all rows (_kernels.py:28-57)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    d = np.ascontiguousarray(d_flat, dtype=np.float64)
+    return lib().mpo_max_violation(_dp(x), _dp(f), _dp(d), n)
+
+
+# ---------------------------------------------------------------------------
+# pure-Python restatement for tiny n (cross-check of the C port)
+# ---------------------------------------------------------------------------
+
+def _pos(n, i, j):
+    return i * (n - 1) - i * (i - 1) // 2 + (j - i - 1)
+
+
+def tiles_of(n, b):
+    """tiled_rounds (schedule.py:117-153) as lists of (x, z)."""
+    rounds = []
+
+    def one(x, z):
+        out, c = [], 0
+        while max(x + c * b, 0) + 2 <= z - c * b:
+            out.append((x + c * b, z - c * b))
+            c += 1
+        return out
+
+    z = n - 1
+    while z >= 2:
+        rounds.append(one(1 - b, z))
+        z -= b
+    x = 1
+    while x + 2 <= n - 1:
+        rounds.append(one(x, n - 1))
+        x += b
+    return rounds
+
+
+def tile_order(n, b, x, z):
+    """Cube order of one tile (schedule.py:156-175)."""
+    klo, ilo = max(z - b + 1, 0), max(x, 0)
+    for jb in range(x + 1, z, b):
+        je = min(jb + b - 1, z - 1)
+        for k in range(klo, z + 1):
+            for j in range(max(jb, 1), min(je, k - 1) + 1):
+                for i in range(ilo, min(x + b - 1, j - 1) + 1):
+                    yield (i, j, k)
+
+
+def visit_order(n, kind, b):
+    if kind == "serial":
+        for i in range(n - 2):
+            for j in range(i + 1, n - 1):
+                for k in range(j + 1, n):
+                    yield (i, j, k)
+        return
+    bb = 1 if kind == "diagonal" else b
+    for rnd in tiles_of(n, bb):
+        for (x, z) in rnd:
+            yield from tile_order(n, bb, x, z)
+
+
+def py_pass(n, eps, x, f, d_flat, winvx, winvf, duals, pair_duals, kind="tiled", b=40):
+    """One pass in reference order; ``duals`` is a dict key->theta (the
+    semantics of the cursor arrays), replaced by this pass's nonzero duals.
+    Returns (viol, new_duals)."""
+    viol = 0.0
+    new = {}
+    for (i, j, k) in visit_order(n, kind, b):
+        pij, pik, pjk = _pos(n, i, j), _pos(n, i, k), _pos(n, j, k)
+        code = ((i * n + j) * n + k) * 3
+        for kd, (pl, m1, m2) in enumerate(((pij, pik, pjk), (pik, pij, pjk), (pjk, pij, pik))):
+            y = duals.get(code + kd, 0.0)
+            d0 = x[pl] - x[m1] - x[m2]
+            if d0 > viol:
+                viol = d0
+            s = winvx[pl] + winvx[m1] + winvx[m2]
+            delta = d0 + y * s / eps
+            theta = eps * delta / s if delta > 0.0 else 0.0
+            coef = (y - theta) / eps
+            if coef != 0.0:
+                x[pl] += coef * winvx[pl]
+                x[m1] -= coef * winvx[m1]
+                x[m2] -= coef * winvx[m2]
+            if theta > THETA_FLOOR:
+                new[code + kd] = theta
+    for p in range(len(x)):
+        d = d_flat[p]
+        s = winvx[p] + winvf[p]
+        for row in (0, 1):
+            y = pair_duals[p, row]
+            d0 = (x[p] - f[p] - d) if row == 0 else (d - x[p] - f[p])
+            if d0 > viol:
+                viol = d0
+            delta = d0 + y * s / eps
+            theta = eps * delta / s if delta > 0.0 else 0.0
+            coef = (y - theta) / eps
+            if coef != 0.0:
+                if row == 0:
+                    x[p] += coef * winvx[p]
+                else:
+                    x[p] -= coef * winvx[p]
+                f[p] -= coef * winvf[p]
+            pair_duals[p, row] = theta if theta > THETA_FLOOR else 0.0
+    return viol, new

@@ -1,0 +1,157 @@
+"""ctypes binding of ``libmetricproj_b200.so`` (the C ABI in
+``include/metricproj_b200.h``).
+
+There is deliberately no fallback: if the shared library is missing, or the
+process has no sm_100 device, every compute entry raises.  ``build()``
+compiles the library in place with nvcc for ``sm_100a``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_DIR = os.path.join(PKG, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libmetricproj_b200.so")
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+
+MP_OK = 0
+MP_ERR_ARG = 1
+MP_ERR_CUDA = 2
+MP_ERR_OOM = 3
+MP_ERR_NONFINITE = 4
+MP_ERR_UNSUPPORTED = 5
+
+SCHEDULE_CODES = {"serial": 0, "diagonal": 1, "tiled": 2}
+MP_FLAG_TIME_ROUNDS = 1
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cuh", ".h", ".cpp")))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/ into _lib/libmetricproj_b200.so (sm_100a)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    deps = sources() + [os.path.join(INCLUDE, "metricproj_b200.h")]
+    if (not force and os.path.exists(LIB_PATH)
+            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(p) for p in deps)):
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
+        nvcc = "/usr/local/cuda/bin/nvcc"
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC,
+           "-o", tmp, os.path.join(CSRC, "mp_solver.cu")]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class MPInstance(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64),
+                ("d_flat", ctypes.POINTER(ctypes.c_double)),
+                ("w_flat", ctypes.POINTER(ctypes.c_double)),
+                ("reg_x", ctypes.POINTER(ctypes.c_double)),
+                ("reg_f", ctypes.POINTER(ctypes.c_double)),
+                ("epsilon", ctypes.c_double)]
+
+
+class MPConfig(ctypes.Structure):
+    _fields_ = [("schedule_kind", ctypes.c_int32),
+                ("tile_b", ctypes.c_int32),
+                ("device", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class MPPassStats(ctypes.Structure):
+    _fields_ = [("pass_index", ctypes.c_int64),
+                ("steps", ctypes.c_int64),
+                ("nnz_metric", ctypes.c_int64),
+                ("primal_objective", ctypes.c_double),
+                ("dual_objective", ctypes.c_double),
+                ("duality_gap", ctypes.c_double),
+                ("max_violation", ctypes.c_double),
+                ("wall_time", ctypes.c_double)]
+
+
+# every symbol include/metricproj_b200.h declares
+EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dual_count",
+           "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
+           "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_last_error", "mp_version")
+
+_lib = None
+
+
+def load():
+    """Load the shared library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: run paper_1901_10084_b200._native.build() "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    D = ctypes.POINTER(ctypes.c_double)
+    I = ctypes.POINTER(ctypes.c_int64)
+    L.mp_create.argtypes = [ctypes.POINTER(MPInstance), ctypes.POINTER(MPConfig),
+                            ctypes.POINTER(P)]
+    L.mp_run_passes.argtypes = [P, ctypes.c_int32, ctypes.POINTER(MPPassStats)]
+    L.mp_get_state.argtypes = [P, D, D]
+    L.mp_set_state.argtypes = [P, D, D]
+    L.mp_dual_count.restype = ctypes.c_int64
+    L.mp_dual_count.argtypes = [P]
+    L.mp_get_duals.argtypes = [P, I, D, D]
+    L.mp_set_duals.argtypes = [P, ctypes.c_int64, I, D, D]
+    L.mp_state_max_violation.argtypes = [P, D]
+    L.mp_get_timing.argtypes = [P, D, D, I]
+    L.mp_flush_l2.argtypes = [P]
+    L.mp_destroy.restype = None
+    L.mp_destroy.argtypes = [P]
+    L.mp_max_violation.argtypes = [ctypes.c_int64, D, D, D, D]
+    L.mp_last_error.restype = ctypes.c_char_p
+    L.mp_version.restype = ctypes.c_char_p
+    for name in ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_get_duals",
+                 "mp_set_duals", "mp_state_max_violation", "mp_get_timing", "mp_flush_l2",
+                 "mp_max_violation"):
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().mp_last_error().decode(errors="replace")
+
+
+def dptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def iptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, message):
+        super().__init__(message)
+        self.code = code
+
+
+def check(code: int, what: str):
+    if code != MP_OK:
+        raise NativeError(code, f"{what}: {last_error()}")

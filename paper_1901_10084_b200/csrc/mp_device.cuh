@@ -1,0 +1,494 @@
+// Device side of the B200 Dykstra triangle sweep.
+//
+// Hot path: the reference's metric_units_pass (_kernels.py:60-132) executed
+// for one round of conflict-free tiles (schedule.tiled_rounds,
+// schedule.py:117-153) as ONE launch, one CTA per tile.
+//
+// Order exactness.  Two triplets conflict iff they share two indices; their
+// index sums L = i+j+k then differ, and inside one round the reference's
+// cube order (k, j, i ascending per j-chunk, _kernels.py:81-131) always
+// visits the conflicting triplet with the smaller L first.
+// Sweeping a tile level by level in L, any order inside a level, is
+// therefore a linear extension of the reference order and reproduces its x
+// bit for bit.  Each CTA walks its tile's L-levels with one __syncthreads()
+// per level; thread slot q owns the pair (i,k) = (ilo + q/b, klo + q%b) and
+// at level L processes the triplet (i, L-i-k, k), all three rows in kind
+// order IJ, IK, JK (_kernels.py:97-109).
+//
+// Shared-memory layout of one tile (R = [ilo,ihi] rows i, K = [klo,z]
+// columns k, J = [jlo,jhi] middle indices):
+//   RK[b][b]      every pair (a,c) with a in R and c in K  (canonical home,
+//                 so x_ij with j in K and x_jk with j in R alias into it)
+//   WR[b][W]      x_ij, i in R, j in J, j < klo  -- ring over j, slot j%W
+//   WK[b][W]      x_jk, j in J, j > ihi, k in K  -- ring over j, slot j%W
+// The rings are streamed from the dense (n x ld) x matrix in j-blocks of
+// BLK columns with cp.async one block ahead of the wavefront, and written
+// back when the wavefront has passed them.  Each pair touched by a tile is
+// touched by no other tile of the round (schedule.py:235-250), so no two
+// CTAs of a launch ever write the same x.
+//
+// Arithmetic mirrors the reference bit for bit: explicit __dadd_rn /
+// __dsub_rn / __dmul_rn / __ddiv_rn (no FMA contraction) in the reference's
+// association (_kernels.py:115-125).  When W = I (reg_x == 1) the weights
+// are exactly 1.0 and s = (1+1)+1 = 3 exactly, so the UNIT specialisation
+// is bitwise identical to the general path.
+//
+// Sparse duals: each warp of each tile owns one "stream" of its nonzero
+// duals, a linked list of 32-entry chunks in a global pool.  Entries are
+// (uint32 key, fp64 theta), key = ((L-Lbeg)*S + slot)*96 + lane*3 + kind,
+// strictly increasing in the warp's own processing order, so the next pass
+// replays them with a single warp cursor (the GPU analogue of the
+// reference's per-worker cursor, _kernels.py:111-114).  Values <=
+// THETA_FLOOR are never stored (_kernels.py:126-129).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mp {
+
+constexpr double THETA_FLOOR = 1e-15;  // _kernels.py:20
+constexpr int BLK = 16;                // j-block width of the streamed rings
+constexpr int CHUNK = 32;              // dual entries per pool chunk
+constexpr uint32_t KEY_END = 0xFFFFFFFFu;
+
+struct TileDesc {
+    int32_t ilo, ihi;  // rows i in [ilo, ihi]            (_kernels.py:76-77)
+    int32_t klo, z;    // columns k in [klo, z]           (_kernels.py:78-80)
+    int32_t jlo, jhi;  // middle j in [jlo, jhi]          (_kernels.py:81-86)
+    int32_t Lbeg, Lend;  // level range of the tile, inclusive
+    int64_t stream0;     // first warp-stream id of the tile
+};
+
+struct DualPool {
+    uint32_t *keys;  // [cap * CHUNK]
+    double *vals;    // [cap * CHUNK]
+    int32_t *next;   // [cap]
+    int32_t *head;   // [nstreams]
+    int32_t cap;
+};
+
+struct PassCounters {
+    unsigned long long viol_bits;  // atomicMax over non-negative doubles
+    unsigned long long nnz;        // metric duals written this pass
+    int32_t chunks_used;
+    int32_t overflow;
+    int32_t nonfinite;
+    int32_t pad;
+};
+
+struct TileArgs {
+    double *x;            // dense n x ld, upper triangle
+    const double *winvx;  // dense n x ld, 1/reg_x (general W only)
+    int64_t ld;
+    const TileDesc *tiles;  // this round's tiles
+    int32_t b;
+    int32_t nt;  // threads per CTA
+    double eps;
+    DualPool rp, wp;
+    PassCounters *ctr;
+};
+
+// ---------------------------------------------------------------------------
+// one metric row, reference association (_kernels.py:115-125)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dykstra_row(double &p, double &m1, double &m2, double wp,
+                                              double wm1, double wm2, double y, double eps,
+                                              double &viol) {
+    const double d0 = __dsub_rn(__dsub_rn(p, m1), m2);
+    viol = d0 > viol ? d0 : viol;
+    const double s = __dadd_rn(__dadd_rn(wp, wm1), wm2);
+    const double delta = __dadd_rn(d0, __ddiv_rn(__dmul_rn(y, s), eps));
+    const double theta = delta > 0.0 ? __ddiv_rn(__dmul_rn(eps, delta), s) : 0.0;
+    const double coef = __ddiv_rn(__dsub_rn(y, theta), eps);
+    if (coef != 0.0) {
+        p = __dadd_rn(p, __dmul_rn(coef, wp));
+        m1 = __dsub_rn(m1, __dmul_rn(coef, wm1));
+        m2 = __dsub_rn(m2, __dmul_rn(coef, wm2));
+    }
+    return theta;
+}
+
+// W = I: every weight is exactly 1.0, coef*1.0 == coef, s == 3.0 exactly.
+__device__ __forceinline__ double dykstra_row_unit(double &p, double &m1, double &m2, double y,
+                                                   double eps, double &viol) {
+    const double d0 = __dsub_rn(__dsub_rn(p, m1), m2);
+    viol = d0 > viol ? d0 : viol;
+    const double s = 3.0;
+    const double delta = __dadd_rn(d0, __ddiv_rn(__dmul_rn(y, s), eps));
+    const double theta = delta > 0.0 ? __ddiv_rn(__dmul_rn(eps, delta), s) : 0.0;
+    const double coef = __ddiv_rn(__dsub_rn(y, theta), eps);
+    if (coef != 0.0) {
+        p = __dadd_rn(p, coef);
+        m1 = __dsub_rn(m1, coef);
+        m2 = __dsub_rn(m2, coef);
+    }
+    return theta;
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long *addr, double v) {
+    // v >= 0: IEEE bit patterns of non-negative doubles order like the values
+    if (v > 0.0) atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// warp-stream reader: replays last pass's duals in processing order
+// ---------------------------------------------------------------------------
+struct StreamReader {
+    uint32_t key;    // this lane's entry of the current chunk
+    double val;
+    uint32_t nkey;   // this lane's entry of the prefetched next chunk
+    double nval;
+    int32_t nnext;   // next pointer of the prefetched chunk
+    int32_t pos;     // first unconsumed entry of the current chunk (warp-uniform)
+    uint32_t head;   // key of entry `pos` (warp-uniform), KEY_END when exhausted
+    bool has_next;   // a prefetched chunk exists (warp-uniform)
+
+    __device__ __forceinline__ void prefetch(const DualPool &p, int32_t c, int lane) {
+        has_next = c >= 0;
+        if (has_next) {
+            nkey = p.keys[(int64_t)c * CHUNK + lane];
+            nval = p.vals[(int64_t)c * CHUNK + lane];
+            nnext = p.next[c];
+        } else {
+            nkey = KEY_END;
+            nval = 0.0;
+            nnext = -1;
+        }
+    }
+    __device__ __forceinline__ void init(const DualPool &p, int64_t stream, int lane) {
+        const int32_t c = p.head[stream];
+        key = KEY_END;
+        val = 0.0;
+        pos = CHUNK;
+        prefetch(p, c, lane);
+        advance(p, lane);
+    }
+    // move to the prefetched chunk (or to the exhausted state)
+    __device__ __forceinline__ void advance(const DualPool &p, int lane) {
+        if (has_next) {
+            key = nkey;
+            val = nval;
+            const int32_t c = nnext;
+            prefetch(p, c, lane);
+            pos = 0;
+            head = __shfl_sync(0xffffffffu, key, 0);
+        } else {
+            key = KEY_END;
+            pos = 0;
+            head = KEY_END;
+        }
+    }
+    // Consume every entry with key in [base, base+96) and hand lane l the
+    // values of its kinds 0..2.
+    __device__ __forceinline__ void lookup(const DualPool &p, uint32_t base, int lane,
+                                           double &y0, double &y1, double &y2) {
+        const uint32_t lim = base + 96u;
+        while (head < lim) {
+            const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && key < lim);
+            unsigned mm = m;
+            while (mm) {
+                const int src = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const uint32_t k = __shfl_sync(0xffffffffu, key, src);
+                const double v = __shfl_sync(0xffffffffu, val, src);
+                const uint32_t off = k - base;
+                if (off / 3u == (uint32_t)lane) {
+                    const uint32_t kd = off - 3u * (uint32_t)lane;
+                    if (kd == 0) y0 = v;
+                    else if (kd == 1) y1 = v;
+                    else y2 = v;
+                }
+            }
+            pos += __popc(m);
+            if (pos >= CHUNK) {
+                advance(p, lane);
+            } else {
+                head = __shfl_sync(0xffffffffu, key, pos);
+            }
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// warp-stream writer: appends this pass's nonzero duals
+// ---------------------------------------------------------------------------
+struct StreamWriter {
+    int32_t chunk;  // current chunk (-1 none yet, -2 dead after overflow); warp-uniform
+    int32_t fill;   // entries used in the current chunk; warp-uniform
+
+    __device__ __forceinline__ void init() {
+        chunk = -1;
+        fill = CHUNK;
+    }
+    __device__ __forceinline__ void append(const DualPool &p, PassCounters *ctr, int64_t stream,
+                                           uint32_t base, int lane, double t0, double t1,
+                                           double t2) {
+        const bool h0 = t0 > THETA_FLOOR, h1 = t1 > THETA_FLOOR, h2 = t2 > THETA_FLOOR;
+        const unsigned m0 = __ballot_sync(0xffffffffu, h0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, h1);
+        const unsigned m2 = __ballot_sync(0xffffffffu, h2);
+        if ((m0 | m1 | m2) == 0u || chunk == -2) return;
+        const unsigned lt = (1u << lane) - 1u;
+        const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
+        const int total = __popc(m0) + __popc(m1) + __popc(m2);
+        const int nnew = (fill + total + CHUNK - 1) / CHUNK - 1;
+        int32_t c0 = 0;
+        if (nnew > 0) {
+            if (lane == 0) {
+                c0 = atomicAdd(&ctr->chunks_used, nnew);
+                if (c0 + nnew > p.cap) {
+                    atomicExch(&ctr->overflow, 1);
+                    c0 = -1;
+                }
+            }
+            c0 = __shfl_sync(0xffffffffu, c0, 0);
+            if (c0 < 0) {
+                chunk = -2;
+                return;
+            }
+            if (lane == 0) {
+                if (chunk >= 0) p.next[chunk] = c0;
+                else p.head[stream] = c0;
+            }
+            if (lane < nnew - 1) p.next[c0 + lane] = c0 + lane + 1;
+        }
+        if (lane == 0) atomicAdd(&ctr->nnz, (unsigned long long)total);
+        int e = fill + before;
+        const double th[3] = {t0, t1, t2};
+        const bool hk[3] = {h0, h1, h2};
+#pragma unroll
+        for (int kd = 0; kd < 3; ++kd) {
+            if (hk[kd]) {
+                const int blk = e / CHUNK;
+                const int32_t c = blk == 0 ? chunk : c0 + blk - 1;
+                const int64_t at = (int64_t)c * CHUNK + (e - blk * CHUNK);
+                p.keys[at] = base + 3u * (uint32_t)lane + (uint32_t)kd;
+                p.vals[at] = th[kd];
+                ++e;
+            }
+        }
+        if (nnew > 0) chunk = c0 + nnew - 1;
+        fill = fill + total - CHUNK * nnew;
+    }
+    __device__ __forceinline__ void finish(const DualPool &p, int64_t stream, int lane) {
+        if (chunk >= 0) {
+            if (lane >= fill) p.keys[(int64_t)chunk * CHUNK + lane] = KEY_END;
+            if (lane == 0) p.next[chunk] = -1;
+        } else if (chunk == -1) {
+            if (lane == 0) p.head[stream] = -1;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// ring staging of the j-window
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Load (LOAD=true, cp.async) or write back (LOAD=false) j-block `blk` of the
+// WR / WK rings for array `g` (x or winvx) into ring arrays `wr`, `wk`.
+// Predicates select exactly the pairs this tile touches that live in the
+// rings (see the layout note above); nothing else is read or written.
+template <int W, bool LOAD>
+__device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld, double *g,
+                                           double *wr, double *wk, int blk, int tid, int nt) {
+    const int j0 = blk * BLK;
+    // WR: rows i in R x 16 columns j (row-contiguous in global memory)
+    const int nwr = b * BLK;
+    for (int e = tid; e < nwr; e += nt) {
+        const int ii = e / BLK, jj = e - ii * BLK;
+        const int i = T.ilo + ii, j = j0 + jj;
+        if (i <= T.ihi && j >= T.jlo && j <= T.jhi && j < T.klo && i < j) {
+            double *s = wr + ii * W + (j & (W - 1));
+            double *gp = g + (int64_t)i * ld + j;
+            if (LOAD) cp_async8(s, gp);
+            else *gp = *s;
+        }
+    }
+    // WK: 16 rows j x columns k in K; a warp covers 4 consecutive k (one
+    // 32-byte sector per row) x 8 rows j
+    const int kq = (b + 3) / 4;
+    const int nwk = kq * 2 * 32;
+    for (int e = tid; e < nwk; e += nt) {
+        const int grp = e >> 5, ln = e & 31;
+        const int kk = (grp % kq) * 4 + (ln & 3);
+        const int jj = (grp / kq) * 8 + (ln >> 2);
+        const int k = T.klo + kk, j = j0 + jj;
+        if (kk < b && k <= T.z && j >= T.jlo && j <= T.jhi && j > T.ihi && j < k) {
+            double *s = wk + kk * W + (j & (W - 1));
+            double *gp = g + (int64_t)j * ld + k;
+            if (LOAD) cp_async8(s, gp);
+            else *gp = *s;
+        }
+    }
+}
+
+// RK block: rows i in R, columns k in K, i < k.
+template <bool LOAD>
+__device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, double *g,
+                                         double *rk, int tid, int nt) {
+    for (int e = tid; e < b * b; e += nt) {
+        const int ii = e / b, kk = e - ii * b;
+        const int i = T.ilo + ii, k = T.klo + kk;
+        if (i <= T.ihi && k <= T.z && i < k) {
+            double *gp = g + (int64_t)i * ld + k;
+            if (LOAD) cp_async8(rk + e, gp);
+            else *gp = rk[e];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the tile kernel: one CTA = one tile of the round
+// ---------------------------------------------------------------------------
+// Largest CTA for S slots per thread (keeps >= 72 registers per thread).
+__host__ __device__ constexpr int max_threads_for(int S) { return S == 1 ? 1024 : (S == 2 ? 832 : 768); }
+
+template <int S, int W, bool UNIT>
+__global__ void __launch_bounds__(max_threads_for(S), 1) tile_round_kernel(TileArgs a) {
+    extern __shared__ __align__(16) double smem[];
+    const TileDesc T = a.tiles[blockIdx.x];
+    const int b = a.b, nt = a.nt, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int bb = b * b;
+    double *RK = smem;
+    double *WR = RK + bb;
+    double *WK = WR + b * W;
+    const int xsize = bb + 2 * b * W;  // doubles of x staging; winv staging follows
+    const double eps = a.eps;
+
+    // --- per-slot geometry --------------------------------------------------
+    int off[S];      // level L is active for the slot iff (unsigned)(L-off) <= span
+    unsigned span[S];
+    int si[S], sk[S];  // i - ilo, k - klo
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int q = tid + s * nt;
+        const int ii = q / b, kk = q - (q / b) * b;
+        const int i = T.ilo + ii, k = T.klo + kk;
+        const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
+        const bool ok = q < bb && i <= T.ihi && k <= T.z && js <= je;
+        si[s] = ii;
+        sk[s] = kk;
+        off[s] = ok ? i + k + js : 0x3fffffff;
+        span[s] = ok ? (unsigned)(je - js) : 0u;
+    }
+
+    // --- staging prologue ---------------------------------------------------
+    // Level L reads j in [L - ihi - z, L - ilo - klo] (clipped to J); keep
+    // those j-blocks landed, one more block in flight, and write blocks back
+    // once the wavefront bottom has passed them.
+    rk_block<true>(T, b, a.ld, a.x, RK, tid, nt);
+    if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt);
+    const int blast = T.jhi / BLK;
+    int lo_res = max(T.Lbeg - T.ihi - T.z, T.jlo) / BLK;  // lowest block not written back
+    int hi_issued = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
+    for (int bk = lo_res; bk <= hi_issued; ++bk) {
+        ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
+        if (!UNIT)
+            ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
+                                bk, tid, nt);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    int hi_landed = hi_issued;
+
+    // --- dual streams --------------------------------------------------------
+    const int64_t stream = T.stream0 + warp;
+    StreamReader rd;
+    rd.init(a.rp, stream, lane);
+    StreamWriter wr;
+    wr.init();
+
+    double viol = 0.0;
+    const int ihi = T.ihi, klo = T.klo, ilo = T.ilo;
+
+    for (int L = T.Lbeg; L <= T.Lend; ++L) {
+        const int need_hi = min(L - ilo - klo, T.jhi) / BLK;
+        if (need_hi > hi_landed) {  // uniform: the wavefront top enters a new block
+            const int low_need = max(L - ihi - T.z, T.jlo) / BLK;
+            for (; lo_res < low_need; ++lo_res)
+                ring_block<W, false>(T, b, a.ld, a.x, WR, WK, lo_res, tid, nt);
+            cp_async_wait_all();
+            __syncthreads();  // landed data visible; write-back reads done
+            hi_landed = hi_issued;
+            if (hi_issued < blast) {
+                ++hi_issued;
+                ring_block<W, true>(T, b, a.ld, a.x, WR, WK, hi_issued, tid, nt);
+                if (!UNIT)
+                    ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize,
+                                        WK + xsize, hi_issued, tid, nt);
+                cp_async_commit();
+            }
+        }
+
+        const uint32_t lbase = (uint32_t)(L - T.Lbeg) * (uint32_t)S;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t base = (lbase + (uint32_t)s) * 96u;
+            double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+            rd.lookup(a.rp, base, lane, y0, y1, y2);
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            if ((unsigned)(L - off[s]) <= span[s]) {
+                const int i = ilo + si[s], k = klo + sk[s];
+                const int j = L - i - k;
+                const int pij = j >= klo ? si[s] * b + (j - klo) : bb + si[s] * W + (j & (W - 1));
+                const int pjk = j <= ihi ? (j - ilo) * b + sk[s]
+                                         : bb + b * W + sk[s] * W + (j & (W - 1));
+                const int pik = si[s] * b + sk[s];
+                double xa = smem[pij], xc = smem[pik], xe = smem[pjk];
+                const double d0 = __dsub_rn(__dsub_rn(xa, xc), xe);
+                const double d1 = __dsub_rn(__dsub_rn(xc, xa), xe);
+                const double d2 = __dsub_rn(__dsub_rn(xe, xa), xc);
+                const bool slow = (y0 != 0.0) | (y1 != 0.0) | (y2 != 0.0) | (d0 > 0.0) |
+                                  (d1 > 0.0) | (d2 > 0.0);
+                if (slow) {
+                    if (UNIT) {
+                        t0 = dykstra_row_unit(xa, xc, xe, y0, eps, viol);  // IJ: x_ij <= x_ik + x_jk
+                        t1 = dykstra_row_unit(xc, xa, xe, y1, eps, viol);  // IK: x_ik <= x_ij + x_jk
+                        t2 = dykstra_row_unit(xe, xa, xc, y2, eps, viol);  // JK: x_jk <= x_ij + x_ik
+                    } else {
+                        const double wa = smem[xsize + pij], wc = smem[xsize + pik],
+                                     we = smem[xsize + pjk];
+                        t0 = dykstra_row(xa, xc, xe, wa, wc, we, y0, eps, viol);
+                        t1 = dykstra_row(xc, xa, xe, wc, wa, we, y1, eps, viol);
+                        t2 = dykstra_row(xe, xa, xc, we, wa, wc, y2, eps, viol);
+                    }
+                    smem[pij] = xa;
+                    smem[pik] = xc;
+                    smem[pjk] = xe;
+                }
+            }
+            wr.append(a.wp, a.ctr, stream, base, lane, t0, t1, t2);
+        }
+        __syncthreads();
+    }
+
+    // --- epilogue: write back everything still staged ------------------------
+    cp_async_wait_all();
+    __syncthreads();
+    for (; lo_res <= hi_issued; ++lo_res)
+        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, lo_res, tid, nt);
+    rk_block<false>(T, b, a.ld, a.x, RK, tid, nt);
+    wr.finish(a.wp, stream, lane);
+    viol = warp_max(viol);
+    if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
+}
+
+}  // namespace mp

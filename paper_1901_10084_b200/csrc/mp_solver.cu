@@ -1,0 +1,829 @@
+// Host side of the B200 Dykstra triangle sweep and the C ABI declared in
+// include/metricproj_b200.h.
+//
+// One mp_handle = one solve session with device-resident state (the whole of
+// PrimalState, DualStore and the instance; core.py:97-256).  A pass
+// (run_pass, solver.py:166-210) is: snapshot -> one tile_round_kernel launch
+// per round of the conflict-free schedule (the reference's barrier between
+// rounds, solver.py:150-151, becomes the launch boundary) -> the fused pair
+// phase + objective reductions -> a 1-CTA finalize -> ~64 bytes of stats to
+// pinned host memory.  The sparse dual pools are double-buffered: pass k
+// reads the pool pass k-1 wrote (SPEC.md "read pass k-1, write pass k").
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "metricproj_b200.h"
+#include "mp_aux.cuh"
+#include "mp_device.cuh"
+
+using namespace mp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? MP_ERR_OOM : MP_ERR_CUDA,     \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                      \
+    } while (0)
+
+int64_t pair_count(int64_t n) { return n * (n - 1) / 2; }
+
+int grid_for(int64_t work, int threads, int cap) {
+    int64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+// Tile geometry (_kernels.py:74-86): rows [max(x,0), x+b-1], columns
+// [max(z-b+1,0), z], middle [max(x+1,1), z-1]; level range of the tile.
+TileDesc make_tile(int64_t x, int64_t z, int64_t b) {
+    TileDesc t{};
+    t.ilo = (int32_t)std::max<int64_t>(x, 0);
+    t.ihi = (int32_t)(x + b - 1);
+    t.klo = (int32_t)std::max<int64_t>(z - b + 1, 0);
+    t.z = (int32_t)z;
+    t.jlo = (int32_t)std::max<int64_t>(x + 1, 1);
+    t.jhi = (int32_t)(z - 1);
+    const int64_t j0 = std::max<int64_t>(t.jlo, t.ilo + 1);
+    const int64_t k0 = std::max<int64_t>(t.klo, j0 + 1);
+    t.Lbeg = (int32_t)(t.ilo + j0 + k0);
+    t.Lend = (int32_t)(std::min<int64_t>(t.ihi, z - 2) + (z - 1) + z);
+    return t;
+}
+
+}  // namespace
+
+struct mp_handle {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    int64_t n = 0, m = 0, ld = 0;
+    int b = 0, kind = 0;
+    uint32_t flags = 0;
+    double eps = 0.0;
+    bool unit_x = true, unit_f = true;
+
+    // device state (x and winvx dense n x ld; the rest packed C(n,2))
+    double *x = nullptr, *winvx = nullptr;
+    double *f = nullptr, *d = nullptr, *w = nullptr, *regx = nullptr, *regf = nullptr,
+           *winvf = nullptr, *pu = nullptr, *pl = nullptr, *tmp = nullptr;
+    double *snap_x = nullptr, *snap_f = nullptr, *snap_pu = nullptr, *snap_pl = nullptr;
+
+    // schedule
+    int S = 1, NT = 32, W = 64;
+    size_t smem = 0;
+    std::vector<TileDesc> tiles;
+    std::vector<int64_t> round_off, round_cnt;
+    std::vector<int64_t> tile_x;      // tile base x per tile (for dual decode)
+    std::vector<int32_t> tile_of_blk; // (iblock, kblock) -> tile index
+    int64_t nib = 0, nkb = 0;
+    TileDesc *d_tiles = nullptr;
+    int64_t nstreams = 0;
+
+    // sparse duals: two pools, pool[rp] holds the previous pass's duals
+    DualPool pool[2]{};
+    int32_t pool_used[2] = {0, 0};
+    int rp = 0;
+    int64_t nnz = 0;
+
+    // per-pass bookkeeping
+    PassCounters *ctr = nullptr;
+    double *partials = nullptr;
+    int pair_grid = 1;
+    DevStats *d_stats = nullptr, *h_stats = nullptr;
+    cudaEvent_t ev[4]{};
+    int64_t pass_index = 0;
+    double metric_ms = 0.0, pair_ms = 0.0;
+    int64_t launches = 0;
+    unsigned long long *d_scan = nullptr;
+    void *flush = nullptr;
+    size_t flush_bytes = 0;
+
+    ~mp_handle() {
+        if (dev >= 0) cudaSetDevice(dev);
+        double *bufs[] = {x, winvx, f, d, w, regx, regf, winvf, pu, pl, tmp,
+                          snap_x, snap_f, snap_pu, snap_pl, partials};
+        for (double *p : bufs)
+            if (p) cudaFree(p);
+        for (auto &p : pool) {
+            cudaFree(p.keys);
+            cudaFree(p.vals);
+            cudaFree(p.next);
+            cudaFree(p.head);
+        }
+        cudaFree(d_tiles);
+        cudaFree(ctr);
+        cudaFree(d_stats);
+        cudaFree(d_scan);
+        cudaFree(flush);
+        if (h_stats) cudaFreeHost(h_stats);
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+int alloc_pool(mp_handle *h, int which, int32_t cap) {
+    DualPool &p = h->pool[which];
+    cudaFree(p.keys);
+    cudaFree(p.vals);
+    cudaFree(p.next);
+    p.keys = nullptr;
+    p.vals = nullptr;
+    p.next = nullptr;
+    CK(cudaMalloc(&p.keys, (size_t)cap * CHUNK * sizeof(uint32_t)));
+    CK(cudaMalloc(&p.vals, (size_t)cap * CHUNK * sizeof(double)));
+    CK(cudaMalloc(&p.next, (size_t)cap * sizeof(int32_t)));
+    p.cap = cap;
+    if (!p.head) {
+        CK(cudaMalloc(&p.head, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
+        CK(cudaMemsetAsync(p.head, 0xff, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t),
+                           h->st));
+    }
+    return MP_OK;
+}
+
+template <int S, int W, bool U>
+int launch_tiles_t(mp_handle *h, const TileArgs &a, int ntiles) {
+    auto k = tile_round_kernel<S, W, U>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    k<<<ntiles, h->NT, h->smem, h->st>>>(a);
+    CK(cudaGetLastError());
+    return MP_OK;
+}
+
+template <int S>
+int launch_tiles_s(mp_handle *h, const TileArgs &a, int ntiles) {
+    if (h->W == 64)
+        return h->unit_x ? launch_tiles_t<S, 64, true>(h, a, ntiles)
+                         : launch_tiles_t<S, 64, false>(h, a, ntiles);
+    return h->unit_x ? launch_tiles_t<S, 128, true>(h, a, ntiles)
+                     : launch_tiles_t<S, 128, false>(h, a, ntiles);
+}
+
+int launch_tiles(mp_handle *h, const TileArgs &a, int ntiles) {
+    switch (h->S) {
+        case 1: return launch_tiles_s<1>(h, a, ntiles);
+        case 2: return launch_tiles_s<2>(h, a, ntiles);
+        default: return launch_tiles_s<3>(h, a, ntiles);
+    }
+}
+
+int launch_pairs(mp_handle *h, const PairArgs &a) {
+    if (h->unit_x && h->unit_f)
+        pair_phase_kernel<true, true><<<h->pair_grid, 256, 0, h->st>>>(a);
+    else if (h->unit_x)
+        pair_phase_kernel<true, false><<<h->pair_grid, 256, 0, h->st>>>(a);
+    else if (h->unit_f)
+        pair_phase_kernel<false, true><<<h->pair_grid, 256, 0, h->st>>>(a);
+    else
+        pair_phase_kernel<false, false><<<h->pair_grid, 256, 0, h->st>>>(a);
+    CK(cudaGetLastError());
+    return MP_OK;
+}
+
+// Enqueue one pass (no host sync).  Returns an MP_* code for launch errors.
+int enqueue_pass(mp_handle *h) {
+    const int wp = h->rp ^ 1;
+    CK(cudaMemsetAsync(h->ctr, 0, sizeof(PassCounters), h->st));
+    // snapshot for an overflow retry of this pass
+    CK(cudaMemcpyAsync(h->snap_x, h->x, (size_t)h->n * h->ld * sizeof(double),
+                       cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->snap_f, h->f, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->snap_pu, h->pu, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->snap_pl, h->pl, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaEventRecord(h->ev[1], h->st));
+    TileArgs ta{};
+    ta.x = h->x;
+    ta.winvx = h->winvx;
+    ta.ld = h->ld;
+    ta.b = h->b;
+    ta.nt = h->NT;
+    ta.eps = h->eps;
+    ta.rp = h->pool[h->rp];
+    ta.wp = h->pool[wp];
+    ta.ctr = h->ctr;
+    for (size_t r = 0; r < h->round_cnt.size(); ++r) {
+        if (!h->round_cnt[r]) continue;
+        ta.tiles = h->d_tiles + h->round_off[r];
+        int rc = launch_tiles(h, ta, (int)h->round_cnt[r]);
+        if (rc) return rc;
+    }
+    CK(cudaEventRecord(h->ev[2], h->st));
+    PairArgs pa{};
+    pa.x = h->x;
+    pa.ld = h->ld;
+    pa.f = h->f;
+    pa.d = h->d;
+    pa.w = h->w;
+    pa.winvx = h->winvx;
+    pa.winvf = h->winvf;
+    pa.regx = h->regx;
+    pa.regf = h->regf;
+    pa.pu = h->pu;
+    pa.pl = h->pl;
+    pa.n = h->n;
+    pa.m = h->m;
+    pa.eps = h->eps;
+    pa.partials = h->partials;
+    pa.ctr = h->ctr;
+    int rc = launch_pairs(h, pa);
+    if (rc) return rc;
+    finalize_kernel<<<1, 1024, 0, h->st>>>(h->partials, h->pair_grid, h->eps, h->ctr, h->d_stats);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev[3], h->st));
+    CK(cudaMemcpyAsync(h->h_stats, h->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, h->st));
+    return MP_OK;
+}
+
+int restore_snapshot(mp_handle *h) {
+    CK(cudaMemcpyAsync(h->x, h->snap_x, (size_t)h->n * h->ld * sizeof(double),
+                       cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->f, h->snap_f, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->pu, h->snap_pu, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->pl, h->snap_pl, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    return MP_OK;
+}
+
+int upload_packed(mp_handle *h, double **dst, const double *src) {
+    CK(cudaMalloc(dst, h->m * sizeof(double)));
+    CK(cudaMemcpyAsync(*dst, src, h->m * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    return MP_OK;
+}
+
+// decode one stored entry of tile t / warp w into the reference key
+struct Decoded {
+    int64_t i, j, k, kind;
+};
+
+Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
+    const TileDesc &T = h->tiles[t];
+    const uint32_t per_level = (uint32_t)h->S * 96u;
+    const uint32_t lvl = key / per_level, rem = key % per_level;
+    const int s = (int)(rem / 96u), r2 = (int)(rem % 96u);
+    const int lane = r2 / 3, kind = r2 % 3;
+    const int64_t q = (int64_t)w * 32 + lane + (int64_t)s * h->NT;
+    const int64_t ii = q / h->b, kk = q % h->b;
+    Decoded d;
+    d.i = T.ilo + ii;
+    d.k = T.klo + kk;
+    d.j = (int64_t)T.Lbeg + lvl - d.i - d.k;
+    d.kind = kind;
+    return d;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *mp_last_error(void) { return g_err.c_str(); }
+
+const char *mp_version(void) { return "metricproj_b200 0.1.0 (sm_100a)"; }
+
+int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
+    g_err.clear();
+    if (!inst || !cfg || !out) return fail(MP_ERR_ARG, "null argument");
+    *out = nullptr;
+    const int64_t n = inst->n;
+    if (n < 3) return fail(MP_ERR_ARG, "need n >= 3, got %lld", (long long)n);
+    if (n > 2000000) return fail(MP_ERR_ARG, "n too large: %lld", (long long)n);
+    if (!(inst->epsilon > 0.0) || !std::isfinite(inst->epsilon))
+        return fail(MP_ERR_ARG, "epsilon must be positive, got %g", inst->epsilon);
+    if (!inst->d_flat || !inst->w_flat) return fail(MP_ERR_ARG, "d_flat / w_flat are required");
+    if (cfg->schedule_kind < 0 || cfg->schedule_kind > 2)
+        return fail(MP_ERR_ARG, "unknown schedule_kind %d", cfg->schedule_kind);
+    if (cfg->schedule_kind == MP_SCHEDULE_SERIAL)
+        return fail(MP_ERR_UNSUPPORTED, "schedule_kind 'serial' is not implemented on the device");
+    const int b = cfg->schedule_kind == MP_SCHEDULE_DIAGONAL ? 1 : cfg->tile_b;
+    if (b < 1) return fail(MP_ERR_ARG, "tile size must be >= 1, got %d", b);
+    if (b > 48) return fail(MP_ERR_UNSUPPORTED, "tile size %d > 48 is not supported on the device", b);
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(MP_ERR_CUDA, "no CUDA device available (%s); there is no CPU fallback",
+                    cudaGetErrorString(e));
+    if (cfg->device < 0 || cfg->device >= ndev)
+        return fail(MP_ERR_ARG, "device %d out of range (%d devices)", cfg->device, ndev);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, cfg->device));
+    if (prop.major != 10)
+        return fail(MP_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", cfg->device,
+                    prop.major, prop.minor);
+
+    mp_handle *h = new mp_handle();
+    h->dev = cfg->device;
+    auto bail = [&](int rc) {
+        delete h;
+        return rc;
+    };
+    if (cudaSetDevice(h->dev) != cudaSuccess) return bail(fail(MP_ERR_CUDA, "cudaSetDevice"));
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(MP_ERR_CUDA, "stream create"));
+    h->n = n;
+    h->m = pair_count(n);
+    h->ld = (n + 31) / 32 * 32;
+    h->b = b;
+    h->kind = cfg->schedule_kind;
+    h->flags = cfg->flags;
+    h->eps = inst->epsilon;
+    const int64_t m = h->m;
+
+    // regularizer checks (core.py:135-140)
+    if (inst->reg_x)
+        for (int64_t p = 0; p < m; ++p) {
+            if (!(inst->reg_x[p] > 0.0)) return bail(fail(MP_ERR_ARG, "regularization weights must be positive"));
+            if (inst->reg_x[p] != 1.0) h->unit_x = false;
+        }
+    if (inst->reg_f)
+        for (int64_t p = 0; p < m; ++p) {
+            if (!(inst->reg_f[p] > 0.0)) return bail(fail(MP_ERR_ARG, "regularization weights must be positive"));
+            if (inst->reg_f[p] != 1.0) h->unit_f = false;
+        }
+
+    // ---- schedule (schedule.tiled_rounds, schedule.py:117-153) -------------
+    for (h->S = 1;; ++h->S) {
+        h->NT = ((b * b + h->S - 1) / h->S + 31) / 32 * 32;
+        if (h->NT <= max_threads_for(h->S)) break;
+    }
+    h->W = b <= 16 ? 64 : 128;
+    const int nwarps = h->NT / 32;
+    h->nib = (n + b - 1) / b + 2;
+    h->nkb = (n - 1) / b + 2;
+    h->tile_of_blk.assign((size_t)(h->nib * h->nkb), -1);
+    auto emit = [&](int64_t x, int64_t z) {
+        h->round_off.push_back((int64_t)h->tiles.size());
+        int64_t cnt = 0;
+        for (int64_t c = 0; std::max<int64_t>(x + c * b, 0) + 2 <= z - c * b; ++c) {
+            const int64_t tx = x + c * b, tz = z - c * b;
+            TileDesc t = make_tile(tx, tz, b);
+            t.stream0 = (int64_t)h->tiles.size() * nwarps;
+            const int64_t iblk = (t.ilo + b - 1) / b, kblk = (n - 1 - tz) / b;
+            h->tile_of_blk[(size_t)(iblk * h->nkb + kblk)] = (int32_t)h->tiles.size();
+            h->tiles.push_back(t);
+            h->tile_x.push_back(tx);
+            ++cnt;
+        }
+        h->round_cnt.push_back(cnt);
+    };
+    for (int64_t z = n - 1; z >= 2; z -= b) emit(1 - b, z);
+    for (int64_t x = 1; x + 2 <= n - 1; x += b) emit(x, n - 1);
+    h->nstreams = (int64_t)h->tiles.size() * nwarps;
+    for (const TileDesc &t : h->tiles) {
+        const uint64_t keys = (uint64_t)(t.Lend - t.Lbeg + 1) * (uint64_t)h->S * 96ull;
+        if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
+    }
+    const size_t xsz = (size_t)b * b + 2 * (size_t)b * h->W;
+    h->smem = xsz * sizeof(double) * (h->unit_x ? 1 : 2);
+    if (h->smem > 227 * 1024) return bail(fail(MP_ERR_UNSUPPORTED, "tile staging needs %zu bytes of shared memory", h->smem));
+
+    int rc;
+#define TRY(call)                        \
+    do {                                 \
+        cudaError_t e_ = (call);         \
+        if (e_ != cudaSuccess) {         \
+            fail(e_ == cudaErrorMemoryAllocation ? MP_ERR_OOM : MP_ERR_CUDA, "%s: %s", #call, \
+                 cudaGetErrorString(e_)); \
+            return bail(e_ == cudaErrorMemoryAllocation ? MP_ERR_OOM : MP_ERR_CUDA); \
+        }                                \
+    } while (0)
+    TRY(cudaMalloc(&h->d_tiles, std::max<size_t>(h->tiles.size(), 1) * sizeof(TileDesc)));
+    TRY(cudaMemcpyAsync(h->d_tiles, h->tiles.data(), h->tiles.size() * sizeof(TileDesc),
+                        cudaMemcpyHostToDevice, h->st));
+
+    // ---- instance and state --------------------------------------------------
+    const size_t dense = (size_t)n * h->ld * sizeof(double);
+    TRY(cudaMalloc(&h->x, dense));
+    TRY(cudaMemsetAsync(h->x, 0, dense, h->st));  // x = 0 (solver.py:112)
+    TRY(cudaMalloc(&h->snap_x, dense));
+    TRY(cudaMalloc(&h->tmp, m * sizeof(double)));
+    if ((rc = upload_packed(h, &h->d, inst->d_flat))) return bail(rc);
+    if ((rc = upload_packed(h, &h->w, inst->w_flat))) return bail(rc);
+    const int egrid = grid_for(m, 256, 148 * 16);
+    if (!h->unit_x) {
+        if ((rc = upload_packed(h, &h->regx, inst->reg_x))) return bail(rc);
+        TRY(cudaMalloc(&h->winvx, dense));
+        reciprocal_kernel<<<egrid, 256, 0, h->st>>>(h->regx, h->tmp, m);  // solver.py:173
+        expand_kernel<<<egrid, 256, 0, h->st>>>(h->tmp, h->winvx, h->ld, n, m);
+        TRY(cudaGetLastError());
+    }
+    if (!h->unit_f) {
+        if ((rc = upload_packed(h, &h->regf, inst->reg_f))) return bail(rc);
+        TRY(cudaMalloc(&h->winvf, m * sizeof(double)));
+        reciprocal_kernel<<<egrid, 256, 0, h->st>>>(h->regf, h->winvf, m);  // solver.py:174
+        TRY(cudaGetLastError());
+    }
+    // f = -w / (eps * reg_f)  (solver.py:112), computed as numpy does
+    {
+        std::vector<double> f0((size_t)m);
+        for (int64_t p = 0; p < m; ++p)
+            f0[(size_t)p] = (-inst->w_flat[p]) / (inst->epsilon * (inst->reg_f ? inst->reg_f[p] : 1.0));
+        if ((rc = upload_packed(h, &h->f, f0.data()))) return bail(rc);
+        TRY(cudaStreamSynchronize(h->st));
+    }
+    TRY(cudaMalloc(&h->pu, m * sizeof(double)));
+    TRY(cudaMalloc(&h->pl, m * sizeof(double)));
+    TRY(cudaMemsetAsync(h->pu, 0, m * sizeof(double), h->st));
+    TRY(cudaMemsetAsync(h->pl, 0, m * sizeof(double), h->st));
+    TRY(cudaMalloc(&h->snap_f, m * sizeof(double)));
+    TRY(cudaMalloc(&h->snap_pu, m * sizeof(double)));
+    TRY(cudaMalloc(&h->snap_pl, m * sizeof(double)));
+
+    // ---- duals and bookkeeping -------------------------------------------------
+    const int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams / 4), 1 << 30);
+    if ((rc = alloc_pool(h, 0, cap0))) return bail(rc);
+    if ((rc = alloc_pool(h, 1, cap0))) return bail(rc);
+    h->pair_grid = grid_for(m, 256, 148 * 8);
+    TRY(cudaMalloc(&h->partials, (size_t)h->pair_grid * 4 * sizeof(double)));
+    TRY(cudaMalloc(&h->ctr, sizeof(PassCounters)));
+    TRY(cudaMalloc(&h->d_stats, sizeof(DevStats)));
+    TRY(cudaMalloc(&h->d_scan, sizeof(unsigned long long)));
+    TRY(cudaMallocHost(&h->h_stats, sizeof(DevStats)));
+    for (auto &ev : h->ev) TRY(cudaEventCreate(&ev));
+    TRY(cudaStreamSynchronize(h->st));
+#undef TRY
+    *out = h;
+    return MP_OK;
+}
+
+void mp_destroy(mp_handle *h) { delete h; }
+
+int mp_run_passes(mp_handle *h, int32_t npasses, mp_pass_stats *out) {
+    g_err.clear();
+    if (!h || npasses < 0 || (npasses > 0 && !out)) return fail(MP_ERR_ARG, "bad argument");
+    CK(cudaSetDevice(h->dev));
+    h->metric_ms = h->pair_ms = 0.0;
+    h->launches = 0;
+    int64_t nlaunch_pass = 2;
+    for (int64_t c : h->round_cnt) nlaunch_pass += c ? 1 : 0;
+    for (int32_t k = 0; k < npasses; ++k) {
+        const int wp = h->rp ^ 1;
+        // keep the write pool comfortably above the last pass's usage
+        const int64_t want = std::max<int64_t>(h->pool[wp].cap, 2 * (int64_t)h->pool_used[h->rp] + 1024);
+        if (want > h->pool[wp].cap) {
+            CK(cudaStreamSynchronize(h->st));
+            int rc = alloc_pool(h, wp, (int32_t)std::min<int64_t>(want, 0x7fffffff / CHUNK));
+            if (rc) return rc;
+        }
+        for (int attempt = 0;; ++attempt) {
+            CK(cudaEventRecord(h->ev[0], h->st));
+            int rc = enqueue_pass(h);
+            if (rc) return rc;
+            CK(cudaStreamSynchronize(h->st));
+            if (!h->h_stats->overflow) break;
+            // dual pool overflow: roll the pass back, grow the pool, redo it
+            rc = restore_snapshot(h);
+            if (rc) return rc;
+            CK(cudaStreamSynchronize(h->st));
+            const int64_t grow = std::max<int64_t>(2 * (int64_t)h->pool[wp].cap,
+                                                   (int64_t)h->h_stats->chunks_used * 2);
+            if (attempt > 8 || grow > 0x7fffffff / CHUNK)
+                return fail(MP_ERR_OOM, "dual pool cannot grow further");
+            rc = alloc_pool(h, wp, (int32_t)grow);
+            if (rc) return rc;
+        }
+        // device time of the pass (snapshot .. finalize), metric vs pair phase
+        float ms_all = 0.f, ms_metric = 0.f, ms_pair = 0.f;
+        CK(cudaEventElapsedTime(&ms_all, h->ev[0], h->ev[3]));
+        CK(cudaEventElapsedTime(&ms_metric, h->ev[1], h->ev[2]));
+        CK(cudaEventElapsedTime(&ms_pair, h->ev[2], h->ev[3]));
+        h->metric_ms += ms_metric;
+        h->pair_ms += ms_pair;
+        h->launches += nlaunch_pass;
+        const DevStats &s = *h->h_stats;
+        mp_pass_stats &o = out[k];
+        o.pass_index = h->pass_index;
+        o.steps = 3 * (h->n * (h->n - 1) * (h->n - 2) / 6) + 2 * h->m;
+        o.nnz_metric = (int64_t)s.nnz;
+        o.primal_objective = s.primal;
+        o.dual_objective = s.dual;
+        o.duality_gap = s.gap;
+        o.max_violation = s.viol;
+        o.wall_time = ms_all * 1e-3;
+        h->pool_used[wp] = s.chunks_used;
+        h->rp = wp;
+        h->nnz = (int64_t)s.nnz;
+        h->pass_index++;
+        if (s.nonfinite) {
+            return fail(MP_ERR_NONFINITE, "non-finite value in state after pass %lld",
+                        (long long)o.pass_index);
+        }
+    }
+    return MP_OK;
+}
+
+int mp_get_state(mp_handle *h, double *xv, double *fv) {
+    g_err.clear();
+    if (!h) return fail(MP_ERR_ARG, "null handle");
+    CK(cudaSetDevice(h->dev));
+    const int g = grid_for(h->m, 256, 148 * 16);
+    if (xv) {
+        pack_kernel<<<g, 256, 0, h->st>>>(h->x, h->tmp, h->ld, h->n, h->m);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(xv, h->tmp, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    if (fv) CK(cudaMemcpyAsync(fv, h->f, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return MP_OK;
+}
+
+int mp_set_state(mp_handle *h, const double *xv, const double *fv) {
+    g_err.clear();
+    if (!h) return fail(MP_ERR_ARG, "null handle");
+    CK(cudaSetDevice(h->dev));
+    const int g = grid_for(h->m, 256, 148 * 16);
+    if (xv) {
+        CK(cudaMemcpyAsync(h->tmp, xv, h->m * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        expand_kernel<<<g, 256, 0, h->st>>>(h->tmp, h->x, h->ld, h->n, h->m);
+        CK(cudaGetLastError());
+    }
+    if (fv) CK(cudaMemcpyAsync(h->f, fv, h->m * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return MP_OK;
+}
+
+int64_t mp_dual_count(mp_handle *h) { return h ? h->nnz : -1; }
+
+int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) {
+    g_err.clear();
+    if (!h) return fail(MP_ERR_ARG, "null handle");
+    CK(cudaSetDevice(h->dev));
+    if (pair_duals) {
+        std::vector<double> a((size_t)h->m), b((size_t)h->m);
+        CK(cudaMemcpyAsync(a.data(), h->pu, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(b.data(), h->pl, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        for (int64_t p = 0; p < h->m; ++p) {
+            pair_duals[2 * p] = a[(size_t)p];
+            pair_duals[2 * p + 1] = b[(size_t)p];
+        }
+    }
+    if (!keys && !vals) return MP_OK;
+    const DualPool &P = h->pool[h->rp];
+    const int64_t used = h->pool_used[h->rp];
+    std::vector<uint32_t> hk((size_t)used * CHUNK);
+    std::vector<double> hv((size_t)used * CHUNK);
+    std::vector<int32_t> hn((size_t)used), hh((size_t)h->nstreams);
+    if (used) {
+        CK(cudaMemcpyAsync(hk.data(), P.keys, hk.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(hv.data(), P.vals, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(hn.data(), P.next, hn.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+    }
+    if (h->nstreams)
+        CK(cudaMemcpyAsync(hh.data(), P.head, hh.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    const int nwarps = h->NT / 32;
+    const int64_t n = h->n;
+    int64_t outpos = 0;
+    struct E {
+        int64_t rank[5];
+        int64_t key;
+        double val;
+    };
+    std::vector<E> ents;
+    for (size_t t = 0; t < h->tiles.size(); ++t) {
+        ents.clear();
+        const int64_t tx = h->tile_x[t];
+        for (int w = 0; w < nwarps; ++w) {
+            int32_t c = used ? hh[(size_t)(h->tiles[t].stream0 + w)] : -1;
+            while (c >= 0 && c < used) {
+                for (int e = 0; e < CHUNK; ++e) {
+                    const uint32_t key = hk[(size_t)c * CHUNK + e];
+                    if (key == KEY_END) break;
+                    Decoded dd = decode_entry(h, (int64_t)t, w, key);
+                    E en;
+                    // reference cube order inside a tile (_kernels.py:81-97)
+                    en.rank[0] = (dd.j - (tx + 1)) / h->b;
+                    en.rank[1] = dd.k;
+                    en.rank[2] = dd.j;
+                    en.rank[3] = dd.i;
+                    en.rank[4] = dd.kind;
+                    en.key = ((dd.i * n + dd.j) * n + dd.k) * 3 + dd.kind;
+                    en.val = hv[(size_t)c * CHUNK + e];
+                    ents.push_back(en);
+                }
+                c = hn[(size_t)c];
+            }
+        }
+        std::sort(ents.begin(), ents.end(), [](const E &a, const E &b) {
+            return std::lexicographical_compare(a.rank, a.rank + 5, b.rank, b.rank + 5);
+        });
+        for (const E &en : ents) {
+            if (outpos >= h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent (count)");
+            if (keys) keys[outpos] = en.key;
+            if (vals) vals[outpos] = en.val;
+            ++outpos;
+        }
+    }
+    if (outpos != h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent: %lld vs %lld",
+                                      (long long)outpos, (long long)h->nnz);
+    return MP_OK;
+}
+
+int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *vals,
+                 const double *pair_duals) {
+    g_err.clear();
+    if (!h || nnz < 0 || (nnz > 0 && (!keys || !vals))) return fail(MP_ERR_ARG, "bad argument");
+    CK(cudaSetDevice(h->dev));
+    const int64_t n = h->n, b = h->b;
+    // bucket entries by warp stream
+    std::vector<std::pair<int64_t, std::pair<uint32_t, double>>> ents;
+    ents.reserve((size_t)nnz);
+    for (int64_t e = 0; e < nnz; ++e) {
+        const int64_t code = keys[e];
+        if (code < 0) return fail(MP_ERR_ARG, "negative dual key");
+        const int64_t kind = code % 3, t3 = code / 3;
+        const int64_t k = t3 % n, j = (t3 / n) % n, i = t3 / (n * n);
+        if (!(i < j && j < k && k < n)) return fail(MP_ERR_ARG, "invalid metric key %lld", (long long)code);
+        if (!(vals[e] > 0.0) || !std::isfinite(vals[e]))
+            return fail(MP_ERR_ARG, "dual values must be positive and finite");
+        const int64_t iblk = (i + b - 1) / b, kblk = (n - 1 - k) / b;
+        if (iblk >= h->nib || kblk >= h->nkb) return fail(MP_ERR_ARG, "key outside schedule");
+        const int32_t t = h->tile_of_blk[(size_t)(iblk * h->nkb + kblk)];
+        if (t < 0) return fail(MP_ERR_ARG, "key outside schedule");
+        const TileDesc &T = h->tiles[(size_t)t];
+        const int64_t q = (i - T.ilo) * b + (k - T.klo);
+        const int64_t s = q / h->NT, tt = q % h->NT;
+        const int64_t w = tt / 32, lane = tt % 32;
+        const int64_t lvl = i + j + k - T.Lbeg;
+        const uint32_t key32 = (uint32_t)(((lvl * h->S + s) * 96) + lane * 3 + kind);
+        ents.push_back({T.stream0 + w, {key32, vals[e]}});
+    }
+    std::sort(ents.begin(), ents.end(), [](const auto &a, const auto &c) {
+        return a.first != c.first ? a.first < c.first : a.second.first < c.second.first;
+    });
+    for (size_t e = 1; e < ents.size(); ++e)
+        if (ents[e].first == ents[e - 1].first && ents[e].second.first == ents[e - 1].second.first)
+            return fail(MP_ERR_ARG, "duplicate dual key");
+    // pack into chunks
+    std::vector<uint32_t> hk;
+    std::vector<double> hv;
+    std::vector<int32_t> hn, hh((size_t)h->nstreams, -1);
+    size_t e = 0;
+    while (e < ents.size()) {
+        const int64_t s = ents[e].first;
+        int32_t prev = -1;
+        size_t cnt = 0;
+        while (e < ents.size() && ents[e].first == s) {
+            if (cnt % CHUNK == 0) {
+                const int32_t c = (int32_t)hn.size();
+                hn.push_back(-1);
+                hk.resize(hk.size() + CHUNK, KEY_END);
+                hv.resize(hv.size() + CHUNK, 0.0);
+                if (prev >= 0) hn[(size_t)prev] = c;
+                else hh[(size_t)s] = c;
+                prev = c;
+            }
+            hk[(size_t)prev * CHUNK + cnt % CHUNK] = ents[e].second.first;
+            hv[(size_t)prev * CHUNK + cnt % CHUNK] = ents[e].second.second;
+            ++cnt;
+            ++e;
+        }
+    }
+    const int32_t used = (int32_t)hn.size();
+    const int rp = h->rp;
+    if (used > h->pool[rp].cap) {
+        int rc = alloc_pool(h, rp, std::max<int32_t>(used * 2, 4096));
+        if (rc) return rc;
+    }
+    DualPool &P = h->pool[rp];
+    if (used) {
+        CK(cudaMemcpyAsync(P.keys, hk.data(), hk.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(P.vals, hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(P.next, hn.data(), hn.size() * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+    }
+    if (h->nstreams)
+        CK(cudaMemcpyAsync(P.head, hh.data(), hh.size() * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+    h->pool_used[rp] = used;
+    h->nnz = nnz;
+    if (pair_duals) {
+        std::vector<double> a((size_t)h->m), c((size_t)h->m);
+        for (int64_t p = 0; p < h->m; ++p) {
+            a[(size_t)p] = pair_duals[2 * p];
+            c[(size_t)p] = pair_duals[2 * p + 1];
+        }
+        CK(cudaMemcpyAsync(h->pu, a.data(), h->m * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(h->pl, c.data(), h->m * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    return MP_OK;
+}
+
+int mp_state_max_violation(mp_handle *h, double *out) {
+    g_err.clear();
+    if (!h || !out) return fail(MP_ERR_ARG, "bad argument");
+    CK(cudaSetDevice(h->dev));
+    CK(cudaMemsetAsync(h->d_scan, 0, sizeof(unsigned long long), h->st));
+    scan_metric_kernel<<<(unsigned)std::max<int64_t>(h->n - 2, 1), 256, 0, h->st>>>(h->x, h->ld, h->n, h->d_scan);
+    CK(cudaGetLastError());
+    scan_pair_kernel<<<grid_for(h->m, 256, 148 * 16), 256, 0, h->st>>>(h->x, h->ld, h->f, h->d, h->n,
+                                                                        h->m, h->d_scan);
+    CK(cudaGetLastError());
+    unsigned long long bits = 0;
+    CK(cudaMemcpyAsync(&bits, h->d_scan, sizeof(bits), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    double v;
+    std::memcpy(&v, &bits, sizeof(v));
+    *out = v;
+    return MP_OK;
+}
+
+int mp_get_timing(mp_handle *h, double *metric_ms, double *pair_ms, int64_t *launches) {
+    if (!h) return fail(MP_ERR_ARG, "null handle");
+    if (metric_ms) *metric_ms = h->metric_ms;
+    if (pair_ms) *pair_ms = h->pair_ms;
+    if (launches) *launches = h->launches;
+    return MP_OK;
+}
+
+int mp_flush_l2(mp_handle *h) {
+    g_err.clear();
+    if (!h) return fail(MP_ERR_ARG, "null handle");
+    CK(cudaSetDevice(h->dev));
+    if (!h->flush) {
+        h->flush_bytes = (size_t)256 << 20;
+        CK(cudaMalloc(&h->flush, h->flush_bytes));
+    }
+    static unsigned char v = 0;
+    CK(cudaMemsetAsync(h->flush, ++v, h->flush_bytes, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return MP_OK;
+}
+
+int mp_max_violation(int64_t n, const double *xv, const double *fv, const double *d_flat,
+                     double *out) {
+    g_err.clear();
+    if (n < 3 || !xv || !fv || !d_flat || !out) return fail(MP_ERR_ARG, "bad argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MP_ERR_CUDA, "no CUDA device available; there is no CPU fallback");
+    const int64_t m = pair_count(n), ld = (n + 31) / 32 * 32;
+    double *dx = nullptr, *px = nullptr, *pf = nullptr, *pd = nullptr;
+    unsigned long long *acc = nullptr;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    auto cleanup = [&]() {
+        cudaFree(dx);
+        cudaFree(px);
+        cudaFree(pf);
+        cudaFree(pd);
+        cudaFree(acc);
+        cudaStreamDestroy(st);
+    };
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc(&dx, (size_t)n * ld * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&px, m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&pf, m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&pd, m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&acc, sizeof(unsigned long long))) != cudaSuccess) {
+        cleanup();
+        return fail(MP_ERR_OOM, "cudaMalloc: %s", cudaGetErrorString(e));
+    }
+    cudaMemcpyAsync(px, xv, m * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(pf, fv, m * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(pd, d_flat, m * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(acc, 0, sizeof(unsigned long long), st);
+    const int g = grid_for(m, 256, 148 * 16);
+    expand_kernel<<<g, 256, 0, st>>>(px, dx, ld, n, m);
+    scan_metric_kernel<<<(unsigned)(n - 2), 256, 0, st>>>(dx, ld, n, acc);
+    scan_pair_kernel<<<g, 256, 0, st>>>(dx, ld, pf, pd, n, m, acc);
+    unsigned long long bits = 0;
+    cudaMemcpyAsync(&bits, acc, sizeof(bits), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    cleanup();
+    if (e != cudaSuccess) return fail(MP_ERR_CUDA, "max_violation: %s", cudaGetErrorString(e));
+    double v;
+    std::memcpy(&v, &bits, sizeof(v));
+    *out = v;
+    return MP_OK;
+}
+
+}  // extern "C"
