@@ -425,10 +425,19 @@ __global__ void __launch_bounds__(max_threads_for(S), 1) tile_round_kernel(TileA
             const int low_need = max(L - ihi - T.z, T.jlo) / BLK;
             for (; lo_res < low_need; ++lo_res)
                 ring_block<W, false>(T, b, a.ld, a.x, WR, WK, lo_res, tid, nt);
+            // catch up if the block needed now was never prefetched
+            for (; hi_issued < need_hi;) {
+                ++hi_issued;
+                ring_block<W, true>(T, b, a.ld, a.x, WR, WK, hi_issued, tid, nt);
+                if (!UNIT)
+                    ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize,
+                                        WK + xsize, hi_issued, tid, nt);
+                cp_async_commit();
+            }
             cp_async_wait_all();
             __syncthreads();  // landed data visible; write-back reads done
             hi_landed = hi_issued;
-            if (hi_issued < blast) {
+            if (hi_issued < blast) {  // prefetch one block ahead of the wavefront
                 ++hi_issued;
                 ring_block<W, true>(T, b, a.ld, a.x, WR, WK, hi_issued, tid, nt);
                 if (!UNIT)
