@@ -1,0 +1,305 @@
+#!/usr/bin/env python3
+"""Benchmark: triangle projections/sec of the Dykstra sweep (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--tile-b 40]
+    python bench.py --impl reference ...        # CPU reference arm (oracle port)
+
+A "step" is one full Dykstra pass (all 3*C(n,3) metric rows in the paper's
+tiled order + the pair phase) over the config's seeded synthetic instance.
+``value`` = K * 3*C(n,3) * N / t with t the device time (CUDA events on the
+library's stream) of the K timed passes, max over ranks; L2 is flushed
+(256 MiB write) before every timed pass.  ``e2e`` is the same metric through
+the public ``solve()`` API from host arrays (instance upload, every pass,
+per-pass stats and the final x/f/duals download inside the wall-clock).
+Multi-GPU (torchrun) runs independent replicas, one per GPU (weak scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "triangle projections/sec (whole box)"
+UNIT = "projections/s"
+
+
+def rows_per_pass(n):
+    return 3 * (n * (n - 1) * (n - 2) // 6)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._drain, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _drain(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config, b):
+    """dram bytes per tile-kernel launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_tile_kernel.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        key = f"config{config}_b{b}"
+        return d.get(key, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def workload_name(spec, b):
+    return (f"config{list_index(spec)}: n={spec.n} {spec.name}, gamma={spec.gamma:g}, "
+            f"lambda={spec.lam:g}, tiled b={b}")
+
+
+def list_index(spec):
+    from paper_1901_10084_b200.instances import CONFIGS
+    for k, v in CONFIGS.items():
+        if v is spec:
+            return k
+    return 0
+
+
+def cpu_sample(inst, b, passes_warm, passes_timed, threads):
+    """Time the CPU oracle (a C port of the reference kernels, threaded like
+    the reference's worker pool) on a bounded sample of the workload."""
+    from oracle import oracle
+    oracle.build()
+    o = oracle.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=b, workers=threads)
+    for _ in range(passes_warm):
+        o.run_pass()
+    t0 = time.perf_counter()
+    for _ in range(passes_timed):
+        o.run_pass()
+    dt = time.perf_counter() - t0
+    o.close()
+    return passes_timed * rows_per_pass(inst.n) / dt, dt
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return 0
+    from paper_1901_10084_b200 import instances
+    spec = instances.CONFIGS[args.config]
+    inst = instances.config_instance(args.config)
+    threads = args.cpu_threads or os.cpu_count() or 1
+    rate, dt = cpu_sample(inst, args.tile_b, args.warmup, args.steps, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
+        "config": {"workload": workload_name(spec, args.tile_b), "n": inst.n, "tile_b": args.tile_b,
+                   "parallelism": f"{threads} CPU threads"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"passes {args.warmup + 1}..{args.warmup + args.steps} of the "
+                                   f"config (after {args.warmup} warm-up passes), oracle/ C port "
+                                   "of _kernels.metric_units_pass + pair_pass"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_1901_10084_b200 import instances, schedule
+    from paper_1901_10084_b200.solver import DeviceSession, SolverConfig, solve
+
+    spec = instances.CONFIGS[args.config]
+    inst = instances.config_instance(args.config)
+    n, b = inst.n, args.tile_b
+    rows = rows_per_pass(n)
+
+    # ---- device-resident timing ------------------------------------------------
+    sess = DeviceSession(inst, "tiled", b, device=local)
+    nnz_hist = [0]
+    for _ in range(args.warmup):
+        nnz_hist.append(sess.run(1)[0].nnz_metric)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_dev, metric_ms, pair_ms, launches, nnz_io = 0.0, 0.0, 0.0, 0, 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            sess.flush_l2()
+            st = sess.run(1)[0]
+            t_dev += st.wall_time
+            m_ms, p_ms, nl = sess.timing()
+            metric_ms += m_ms
+            pair_ms += p_ms
+            launches += nl
+            nnz_io += nnz_hist[-1] + st.nnz_metric  # duals read + written
+            nnz_hist.append(st.nnz_metric)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+        tt = torch.tensor([t_dev, metric_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_dev, metric_ms = float(tt[0]), float(tt[1])
+    sess.close()
+    value = ws * args.steps * rows / t_dev
+
+    # ---- roofline of the dominant kernel (tile_round_kernel) ------------------
+    tx = schedule.touched_pairs(n, b)
+    metric_bytes = args.steps * 16 * tx + 12 * nnz_io  # x read+write per touched pair, 12 B/dual
+    achieved = metric_bytes / (metric_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    n_rounds = sum(1 for r in schedule.tiled_rounds(n, b) if r.units)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(args.config, b),
+                "kernel": "tile_round_kernel", "peak_source": peak_src,
+                "frac_of_8TBs_nominal": achieved / 8000.0,
+                "algorithmic_bytes_per_pass": 16 * tx + 12 * nnz_io / max(args.steps, 1),
+                "T_x": tx, "metric_phase_share": metric_ms / (t_dev * 1e3),
+                "launches_per_pass": n_rounds + 2,
+                "critical_levels_per_pass": schedule.critical_levels(n, b),
+                "ns_per_level": metric_ms * 1e6 / args.steps / schedule.critical_levels(n, b)}
+
+    # ---- end to end through the public API (host buffers) ---------------------
+    total = args.warmup + args.steps
+    if ws > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    sol = solve(inst, SolverConfig(tile_size=b, fixed_passes=total, device=local))
+    t_e2e = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    m = inst.npairs
+    h2d = 8 * 4 * m  # d, w, reg_x, reg_f
+    d2h = total * 64 + 8 * 2 * m + 16 * m + 16 * sol.duals.nnz()
+    e2e = {"value": ws * total * rows / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": h2d / total, "d2h_bytes_per_step": d2h / total,
+           "wall_s": t_e2e, "passes": total}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = args.cpu_threads or os.cpu_count() or 1
+        warm, timed = (2, 3) if n <= 1500 else (1, 1)
+        rate, dt = cpu_sample(inst, b, warm, timed, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"passes {warm + 1}..{warm + timed} of the same instance after {warm} "
+                         f"warm-up passes ({dt:.1f} s), oracle/ C port of the reference kernels, "
+                         f"{threads} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator with the BASELINE config shape)",
+            "config": {"workload": workload_name(spec, b), "n": n, "tile_b": b,
+                       "passes_in_config": spec.passes,
+                       "l2": "flushed (256 MiB write) before every timed pass",
+                       "parallelism": "replicas" if ws > 1 else "1 GPU"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "final": {"primal": sol.stats[-1].primal_objective,
+                      "max_violation": sol.stats[-1].max_violation, "nnz": sol.duals.nnz()},
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--tile-b", type=int, default=40)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -27,6 +27,15 @@
 // touched by no other tile of the round (schedule.py:235-250), so no two
 // CTAs of a launch ever write the same x.
 //
+// Hot / cold split.  In the common case a row is neither violated nor has a
+// stored dual, and the reference step is then a no-op (delta = d0 <= 0 ->
+// theta = coef = 0).  The hot loop therefore only loads the three x values,
+// forms the three row values with six DADDs and tests them; a warp that
+// finds a violated row or reaches a stored dual calls the out-of-line
+// cold_level(), which replays the level for its slots with the full
+// reference step.  Keeping the IEEE divisions and the dual bookkeeping out
+// of line keeps the hot loop's register footprint small.
+//
 // Arithmetic mirrors the reference bit for bit: explicit __dadd_rn /
 // __dsub_rn / __dmul_rn / __ddiv_rn (no FMA contraction) in the reference's
 // association (_kernels.py:115-125).  When W = I (reg_x == 1) the weights
@@ -34,12 +43,14 @@
 // is bitwise identical to the general path.
 //
 // Sparse duals: each warp of each tile owns one "stream" of its nonzero
-// duals, a linked list of 32-entry chunks in a global pool.  Entries are
-// (uint32 key, fp64 theta), key = ((L-Lbeg)*S + slot)*96 + lane*3 + kind,
-// strictly increasing in the warp's own processing order, so the next pass
-// replays them with a single warp cursor (the GPU analogue of the
-// reference's per-worker cursor, _kernels.py:111-114).  Values <=
-// THETA_FLOOR are never stored (_kernels.py:126-129).
+// duals, a linked list of 32-entry chunk records in a global pool.  Entries
+// are (uint32 key, fp64 theta), key = ((L-Lbeg)*S + slot)*96 + lane*3 +
+// kind, strictly increasing in the warp's own processing order, so the next
+// pass replays them with a single warp cursor (the GPU analogue of the
+// reference's per-worker cursor, _kernels.py:111-114).  The reader keeps
+// the current and the next chunk in shared memory, the next one in flight
+// as a bulk async copy (cp.async.bulk + mbarrier).  Values <= THETA_FLOOR
+// are never stored (_kernels.py:126-129).
 #pragma once
 
 #include <cstdint>
@@ -51,20 +62,28 @@ constexpr double THETA_FLOOR = 1e-15;  // _kernels.py:20
 constexpr int BLK = 16;                // j-block width of the streamed rings
 constexpr int CHUNK = 32;              // dual entries per pool chunk
 constexpr uint32_t KEY_END = 0xFFFFFFFFu;
+constexpr int MAX_CTA_THREADS = 512;   // >= 128 registers per thread
+constexpr int MAX_SLOTS = 5;           // b <= 50 at 512 threads
 
 struct TileDesc {
-    int32_t ilo, ihi;  // rows i in [ilo, ihi]            (_kernels.py:76-77)
-    int32_t klo, z;    // columns k in [klo, z]           (_kernels.py:78-80)
-    int32_t jlo, jhi;  // middle j in [jlo, jhi]          (_kernels.py:81-86)
+    int32_t ilo, ihi;    // rows i in [ilo, ihi]            (_kernels.py:76-77)
+    int32_t klo, z;      // columns k in [klo, z]           (_kernels.py:78-80)
+    int32_t jlo, jhi;    // middle j in [jlo, jhi]          (_kernels.py:81-86)
     int32_t Lbeg, Lend;  // level range of the tile, inclusive
     int64_t stream0;     // first warp-stream id of the tile
 };
 
+struct alignas(16) ChunkRec {
+    uint32_t keys[CHUNK];  // KEY_END past the last entry
+    double vals[CHUNK];
+    int32_t next;          // next chunk of the stream, -1 at the end
+    int32_t pad[3];
+};
+static_assert(sizeof(ChunkRec) == 400, "chunk record layout");
+
 struct DualPool {
-    uint32_t *keys;  // [cap * CHUNK]
-    double *vals;    // [cap * CHUNK]
-    int32_t *next;   // [cap]
-    int32_t *head;   // [nstreams]
+    ChunkRec *rec;  // [cap]
+    int32_t *head;  // [nstreams] first chunk of each warp stream, -1 if empty
     int32_t cap;
 };
 
@@ -87,41 +106,62 @@ struct TileArgs {
     double eps;
     DualPool rp, wp;
     PassCounters *ctr;
+    int32_t dbg;  // TEMP experiment switches
+};
+
+// Per-warp dual-stream state, in shared memory.
+struct alignas(16) WarpDuals {
+    ChunkRec buf[2];               // current / next chunk of the read stream
+    unsigned long long mbar[2];    // completion of the bulk copy into buf[b]
+    uint32_t phase[2];             // parity to wait for next, per buffer
+    int32_t cur, pos;              // current buffer, first unconsumed entry
+    int32_t has_next;              // buf[cur^1] holds (or receives) the next chunk
+    uint32_t head;                 // key of the next unconsumed entry
+    int32_t wchunk, wfill;         // writer: current chunk (-1 none, -2 dead), fill
+    uint32_t wcount;               // entries written by this warp
+    int32_t pad;
+};
+
+// Per-CTA constants, in shared memory (read by the out-of-line code).
+struct CtaConst {
+    TileDesc T;
+    double *x;
+    const double *winvx;
+    int64_t ld;
+    double eps;
+    DualPool rp, wp;
+    PassCounters *ctr;
+    int32_t b, nt, xsize, dbg;
 };
 
 // ---------------------------------------------------------------------------
 // one metric row, reference association (_kernels.py:115-125)
 // ---------------------------------------------------------------------------
+// Divisions whose value is known exactly are skipped: with y = 0,
+// y*s/eps = +0 and delta = d0 (+0), so d0 <= 0 means theta = coef = 0 (no
+// move, nothing stored) -- the same values the reference computes.
+template <bool UNIT>
 __device__ __forceinline__ double dykstra_row(double &p, double &m1, double &m2, double wp,
                                               double wm1, double wm2, double y, double eps,
                                               double &viol) {
     const double d0 = __dsub_rn(__dsub_rn(p, m1), m2);
     viol = d0 > viol ? d0 : viol;
-    const double s = __dadd_rn(__dadd_rn(wp, wm1), wm2);
-    const double delta = __dadd_rn(d0, __ddiv_rn(__dmul_rn(y, s), eps));
-    const double theta = delta > 0.0 ? __ddiv_rn(__dmul_rn(eps, delta), s) : 0.0;
+    if (y == 0.0 && !(d0 > 0.0)) return 0.0;
+    const double s = UNIT ? 3.0 : __dadd_rn(__dadd_rn(wp, wm1), wm2);
+    const double delta = y == 0.0 ? d0 : __dadd_rn(d0, __ddiv_rn(__dmul_rn(y, s), eps));
+    double theta = 0.0;
+    if (delta > 0.0) theta = __ddiv_rn(__dmul_rn(eps, delta), s);
     const double coef = __ddiv_rn(__dsub_rn(y, theta), eps);
     if (coef != 0.0) {
-        p = __dadd_rn(p, __dmul_rn(coef, wp));
-        m1 = __dsub_rn(m1, __dmul_rn(coef, wm1));
-        m2 = __dsub_rn(m2, __dmul_rn(coef, wm2));
-    }
-    return theta;
-}
-
-// W = I: every weight is exactly 1.0, coef*1.0 == coef, s == 3.0 exactly.
-__device__ __forceinline__ double dykstra_row_unit(double &p, double &m1, double &m2, double y,
-                                                   double eps, double &viol) {
-    const double d0 = __dsub_rn(__dsub_rn(p, m1), m2);
-    viol = d0 > viol ? d0 : viol;
-    const double s = 3.0;
-    const double delta = __dadd_rn(d0, __ddiv_rn(__dmul_rn(y, s), eps));
-    const double theta = delta > 0.0 ? __ddiv_rn(__dmul_rn(eps, delta), s) : 0.0;
-    const double coef = __ddiv_rn(__dsub_rn(y, theta), eps);
-    if (coef != 0.0) {
-        p = __dadd_rn(p, coef);
-        m1 = __dsub_rn(m1, coef);
-        m2 = __dsub_rn(m2, coef);
+        if (UNIT) {
+            p = __dadd_rn(p, coef);
+            m1 = __dsub_rn(m1, coef);
+            m2 = __dsub_rn(m2, coef);
+        } else {
+            p = __dadd_rn(p, __dmul_rn(coef, wp));
+            m1 = __dsub_rn(m1, __dmul_rn(coef, wm1));
+            m2 = __dsub_rn(m2, __dmul_rn(coef, wm2));
+        }
     }
     return theta;
 }
@@ -141,165 +181,218 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // ---------------------------------------------------------------------------
-// warp-stream reader: replays last pass's duals in processing order
+// async copy primitives
 // ---------------------------------------------------------------------------
-struct StreamReader {
-    uint32_t key;    // this lane's entry of the current chunk
-    double val;
-    uint32_t nkey;   // this lane's entry of the prefetched next chunk
-    double nval;
-    int32_t nnext;   // next pointer of the prefetched chunk
-    int32_t pos;     // first unconsumed entry of the current chunk (warp-uniform)
-    uint32_t head;   // key of entry `pos` (warp-uniform), KEY_END when exhausted
-    bool has_next;   // a prefetched chunk exists (warp-uniform)
-
-    __device__ __forceinline__ void prefetch(const DualPool &p, int32_t c, int lane) {
-        has_next = c >= 0;
-        if (has_next) {
-            nkey = p.keys[(int64_t)c * CHUNK + lane];
-            nval = p.vals[(int64_t)c * CHUNK + lane];
-            nnext = p.next[c];
-        } else {
-            nkey = KEY_END;
-            nval = 0.0;
-            nnext = -1;
-        }
-    }
-    __device__ __forceinline__ void init(const DualPool &p, int64_t stream, int lane) {
-        const int32_t c = p.head[stream];
-        key = KEY_END;
-        val = 0.0;
-        pos = CHUNK;
-        prefetch(p, c, lane);
-        advance(p, lane);
-    }
-    // move to the prefetched chunk (or to the exhausted state)
-    __device__ __forceinline__ void advance(const DualPool &p, int lane) {
-        if (has_next) {
-            key = nkey;
-            val = nval;
-            const int32_t c = nnext;
-            prefetch(p, c, lane);
-            pos = 0;
-            head = __shfl_sync(0xffffffffu, key, 0);
-        } else {
-            key = KEY_END;
-            pos = 0;
-            head = KEY_END;
-        }
-    }
-    // Consume every entry with key in [base, base+96) and hand lane l the
-    // values of its kinds 0..2.
-    __device__ __forceinline__ void lookup(const DualPool &p, uint32_t base, int lane,
-                                           double &y0, double &y1, double &y2) {
-        const uint32_t lim = base + 96u;
-        while (head < lim) {
-            const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && key < lim);
-            unsigned mm = m;
-            while (mm) {
-                const int src = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const uint32_t k = __shfl_sync(0xffffffffu, key, src);
-                const double v = __shfl_sync(0xffffffffu, val, src);
-                const uint32_t off = k - base;
-                if (off / 3u == (uint32_t)lane) {
-                    const uint32_t kd = off - 3u * (uint32_t)lane;
-                    if (kd == 0) y0 = v;
-                    else if (kd == 1) y1 = v;
-                    else y2 = v;
-                }
-            }
-            pos += __popc(m);
-            if (pos >= CHUNK) {
-                advance(p, lane);
-            } else {
-                head = __shfl_sync(0xffffffffu, key, pos);
-            }
-        }
-    }
-};
-
-// ---------------------------------------------------------------------------
-// warp-stream writer: appends this pass's nonzero duals
-// ---------------------------------------------------------------------------
-struct StreamWriter {
-    int32_t chunk;  // current chunk (-1 none yet, -2 dead after overflow); warp-uniform
-    int32_t fill;   // entries used in the current chunk; warp-uniform
-
-    __device__ __forceinline__ void init() {
-        chunk = -1;
-        fill = CHUNK;
-    }
-    __device__ __forceinline__ void append(const DualPool &p, PassCounters *ctr, int64_t stream,
-                                           uint32_t base, int lane, double t0, double t1,
-                                           double t2) {
-        const bool h0 = t0 > THETA_FLOOR, h1 = t1 > THETA_FLOOR, h2 = t2 > THETA_FLOOR;
-        const unsigned m0 = __ballot_sync(0xffffffffu, h0);
-        const unsigned m1 = __ballot_sync(0xffffffffu, h1);
-        const unsigned m2 = __ballot_sync(0xffffffffu, h2);
-        if ((m0 | m1 | m2) == 0u || chunk == -2) return;
-        const unsigned lt = (1u << lane) - 1u;
-        const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
-        const int total = __popc(m0) + __popc(m1) + __popc(m2);
-        const int nnew = (fill + total + CHUNK - 1) / CHUNK - 1;
-        int32_t c0 = 0;
-        if (nnew > 0) {
-            if (lane == 0) {
-                c0 = atomicAdd(&ctr->chunks_used, nnew);
-                if (c0 + nnew > p.cap) {
-                    atomicExch(&ctr->overflow, 1);
-                    c0 = -1;
-                }
-            }
-            c0 = __shfl_sync(0xffffffffu, c0, 0);
-            if (c0 < 0) {
-                chunk = -2;
-                return;
-            }
-            if (lane == 0) {
-                if (chunk >= 0) p.next[chunk] = c0;
-                else p.head[stream] = c0;
-            }
-            if (lane < nnew - 1) p.next[c0 + lane] = c0 + lane + 1;
-        }
-        if (lane == 0) atomicAdd(&ctr->nnz, (unsigned long long)total);
-        int e = fill + before;
-        const double th[3] = {t0, t1, t2};
-        const bool hk[3] = {h0, h1, h2};
-#pragma unroll
-        for (int kd = 0; kd < 3; ++kd) {
-            if (hk[kd]) {
-                const int blk = e / CHUNK;
-                const int32_t c = blk == 0 ? chunk : c0 + blk - 1;
-                const int64_t at = (int64_t)c * CHUNK + (e - blk * CHUNK);
-                p.keys[at] = base + 3u * (uint32_t)lane + (uint32_t)kd;
-                p.vals[at] = th[kd];
-                ++e;
-            }
-        }
-        if (nnew > 0) chunk = c0 + nnew - 1;
-        fill = fill + total - CHUNK * nnew;
-    }
-    __device__ __forceinline__ void finish(const DualPool &p, int64_t stream, int lane) {
-        if (chunk >= 0) {
-            if (lane >= fill) p.keys[(int64_t)chunk * CHUNK + lane] = KEY_END;
-            if (lane == 0) p.next[chunk] = -1;
-        } else if (chunk == -1) {
-            if (lane == 0) p.head[stream] = -1;
-        }
-    }
-};
-
-// ---------------------------------------------------------------------------
-// ring staging of the j-window
-// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+// one elected lane: arm the barrier for `bytes` and start the bulk copy
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes,
+                                          unsigned long long *bar) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// warp-stream reader (shared-memory staged, bulk-copy prefetch)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void rd_wait_buf(WarpDuals *w, int bf, int lane) {
+    const uint32_t ph = w->phase[bf];
+    mbar_wait(&w->mbar[bf], ph);
+    __syncwarp();
+    if (lane == 0) w->phase[bf] = ph ^ 1u;
+    __syncwarp();
+}
+
+// Start of a tile: load the stream's first chunk, prefetch the second.
+__device__ __forceinline__ void rd_init(WarpDuals *w, const DualPool &p, int64_t stream,
+                                        int lane) {
+    if (lane == 0) {
+        mbar_init(&w->mbar[0], 1);
+        mbar_init(&w->mbar[1], 1);
+        w->phase[0] = w->phase[1] = 0;
+        w->cur = 0;
+        w->pos = 0;
+        w->wchunk = -1;
+        w->wfill = CHUNK;
+        w->wcount = 0;
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const int32_t c = p.head[stream];
+    if (c >= 0) {
+        if (lane == 0) bulk_load(&w->buf[0], &p.rec[c], sizeof(ChunkRec), &w->mbar[0]);
+        rd_wait_buf(w, 0, lane);
+        const int32_t nx = w->buf[0].next;
+        if (lane == 0) {
+            w->has_next = nx >= 0;
+            if (nx >= 0) bulk_load(&w->buf[1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[1]);
+            w->head = w->buf[0].keys[0];
+        }
+    } else if (lane == 0) {
+        w->has_next = 0;
+        w->head = KEY_END;
+        w->pos = CHUNK;
+    }
+    __syncwarp();
+}
+
+// Consume every entry with key in [base, base+96); lane l receives the values
+// of its kinds 0..2.  Warp-collective.
+__device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint32_t base, int lane,
+                                          double &y0, double &y1, double &y2) {
+    const uint32_t lim = base + 96u;
+    uint32_t head = w->head;
+    int pos = w->pos, cur = w->cur;
+    while (head < lim) {
+        const uint32_t key = w->buf[cur].keys[lane];
+        const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && key < lim);
+        unsigned mm = m;
+        while (mm) {
+            const int src = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const uint32_t off = w->buf[cur].keys[src] - base;
+            if (off / 3u == (uint32_t)lane) {
+                const double v = w->buf[cur].vals[src];
+                const uint32_t kd = off - 3u * (uint32_t)lane;
+                if (kd == 0) y0 = v;
+                else if (kd == 1) y1 = v;
+                else y2 = v;
+            }
+        }
+        pos += __popc(m);
+        if (pos >= CHUNK) {
+            if (!w->has_next) {
+                head = KEY_END;
+                break;
+            }
+            rd_wait_buf(w, cur ^ 1, lane);
+            cur ^= 1;
+            pos = 0;
+            const int32_t nx = w->buf[cur].next;
+            __syncwarp();  // everyone is done with the old buffer
+            if (lane == 0) {
+                w->has_next = nx >= 0;
+                if (nx >= 0) bulk_load(&w->buf[cur ^ 1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[cur ^ 1]);
+            }
+            __syncwarp();
+        }
+        head = w->buf[cur].keys[pos];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        w->head = head;
+        w->pos = pos;
+        w->cur = cur;
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// warp-stream writer: appends this pass's nonzero duals
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassCounters *ctr,
+                                          int64_t stream, uint32_t base, int lane, double t0,
+                                          double t1, double t2) {
+    const bool h0 = t0 > THETA_FLOOR, h1 = t1 > THETA_FLOOR, h2 = t2 > THETA_FLOOR;
+    const unsigned m0 = __ballot_sync(0xffffffffu, h0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, h1);
+    const unsigned m2 = __ballot_sync(0xffffffffu, h2);
+    int32_t chunk = w->wchunk;
+    const int32_t fill = w->wfill;
+    if ((m0 | m1 | m2) == 0u || chunk == -2) return;
+    const unsigned lt = (1u << lane) - 1u;
+    const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
+    const int total = __popc(m0) + __popc(m1) + __popc(m2);
+    const int nnew = (fill + total + CHUNK - 1) / CHUNK - 1;
+    int32_t c0 = 0;
+    if (nnew > 0) {
+        if (lane == 0) {
+            c0 = atomicAdd(&ctr->chunks_used, nnew);
+            if (c0 + nnew > p.cap) {
+                atomicExch(&ctr->overflow, 1);
+                c0 = -1;
+            }
+        }
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        if (c0 < 0) {
+            __syncwarp();
+            if (lane == 0) w->wchunk = -2;
+            __syncwarp();
+            return;
+        }
+        if (lane == 0) {
+            if (chunk >= 0) p.rec[chunk].next = c0;
+            else p.head[stream] = c0;
+        }
+        if (lane < nnew - 1) p.rec[c0 + lane].next = c0 + lane + 1;
+    }
+    int e = fill + before;
+    const double th[3] = {t0, t1, t2};
+    const bool hk[3] = {h0, h1, h2};
+#pragma unroll
+    for (int kd = 0; kd < 3; ++kd) {
+        if (hk[kd]) {
+            const int blk = e / CHUNK;
+            const int32_t c = blk == 0 ? chunk : c0 + blk - 1;
+            p.rec[c].keys[e - blk * CHUNK] = base + 3u * (uint32_t)lane + (uint32_t)kd;
+            p.rec[c].vals[e - blk * CHUNK] = th[kd];
+            ++e;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        w->wchunk = nnew > 0 ? c0 + nnew - 1 : chunk;
+        w->wfill = fill + total - CHUNK * nnew;
+        w->wcount += (uint32_t)total;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void wr_finish(WarpDuals *w, const DualPool &p, PassCounters *ctr,
+                                          int64_t stream, int lane) {
+    const int32_t chunk = w->wchunk, fill = w->wfill;
+    if (lane == 0 && w->wcount) atomicAdd(&ctr->nnz, (unsigned long long)w->wcount);
+    if (chunk >= 0) {
+        if (lane >= fill) p.rec[chunk].keys[lane] = KEY_END;
+        if (lane == 0) p.rec[chunk].next = -1;
+    } else if (chunk == -1) {
+        if (lane == 0) p.head[stream] = -1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ring staging of the j-window
+// ---------------------------------------------------------------------------
 // Load (LOAD=true, cp.async) or write back (LOAD=false) j-block `blk` of the
 // WR / WK rings for array `g` (x or winvx) into ring arrays `wr`, `wk`.
 // Predicates select exactly the pairs this tile touches that live in the
@@ -353,29 +446,262 @@ __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, d
     }
 }
 
+// Ring bookkeeping (CTA-uniform), kept in shared memory.
+struct RingState {
+    int32_t lo_res;     // lowest block not yet written back
+    int32_t hi_issued;  // highest block whose copy was issued
+    int32_t hi_landed;  // highest block known landed
+    int32_t blast;      // last block of J
+};
+
+// Called by the whole CTA when the wavefront top enters a block that has not
+// landed: write back passed blocks, land the needed one, prefetch the next.
+// Returns the level at which this must run again.
+template <int W, bool UNIT>
+__device__ __noinline__ int ring_step(double *smem, const CtaConst *cc, RingState *rs, int L) {
+    const TileDesc &T = cc->T;
+    const int b = cc->b, nt = cc->nt, tid = threadIdx.x, xsize = cc->xsize;
+    double *WR = smem, *WK = smem + b * W;  // SmemMap layout
+    const int need_hi = min(L - T.ilo - T.klo, T.jhi) / BLK;
+    const int low_need = max(L - T.ihi - T.z, T.jlo) / BLK;
+    int lo_res = rs->lo_res, hi_issued = rs->hi_issued;
+    const int blast = rs->blast;
+    for (; lo_res < low_need; ++lo_res)
+        ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, tid, nt);
+    for (; hi_issued < need_hi;) {  // catch up if the needed block was never prefetched
+        ++hi_issued;
+        ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, tid, nt);
+        if (!UNIT)
+            ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
+                                WK + xsize, hi_issued, tid, nt);
+        cp_async_commit();
+    }
+    cp_async_wait_all();
+    __syncthreads();  // landed data visible; write-back reads done; rs read by all
+    const int hi_landed = hi_issued;
+    if (hi_issued < blast) {  // prefetch one block ahead of the wavefront
+        ++hi_issued;
+        ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, tid, nt);
+        if (!UNIT)
+            ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
+                                WK + xsize, hi_issued, tid, nt);
+        cp_async_commit();
+    }
+    __syncthreads();  // everyone has read rs
+    if (tid == 0) {
+        rs->lo_res = lo_res;
+        rs->hi_issued = hi_issued;
+        rs->hi_landed = hi_landed;
+    }
+    // next time the top j = L - ilo - klo leaves block hi_landed
+    return BLK * (hi_landed + 1) + T.ilo + T.klo;
+}
+
+// ---------------------------------------------------------------------------
+// cold path: a warp replays one slot of one level with the full step
+// ---------------------------------------------------------------------------
+// pa/pc/pe are the byte offsets of x_ij, x_ik, x_jk the hot path computed
+// (the zero row for inactive slots, where every row value is 0 and no dual
+// exists, so the exact step is a no-op there).
+template <int W, bool UNIT>
+__device__ __noinline__ double cold_slot(unsigned char *sm, const CtaConst *cc, WarpDuals *wd,
+                                         uint32_t base, int pa, int pc, int pe, double viol) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    if (wd->head < base + 96u) rd_lookup(wd, cc->rp, base, lane, y0, y1, y2);
+    double *xa = reinterpret_cast<double *>(sm + pa);
+    double *xc = reinterpret_cast<double *>(sm + pc);
+    double *xe = reinterpret_cast<double *>(sm + pe);
+    double p = *xa, c = *xc, e = *xe;
+    const double d0 = __dsub_rn(__dsub_rn(p, c), e);
+    const double d1 = __dsub_rn(__dsub_rn(c, p), e);
+    const double d2 = __dsub_rn(__dsub_rn(e, p), c);
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    if ((d0 > 0.0) | (d1 > 0.0) | (d2 > 0.0) | (y0 != 0.0) | (y1 != 0.0) | (y2 != 0.0)) {
+        double wa = 1.0, wc = 1.0, we = 1.0;
+        if (!UNIT) {
+            const int xb = cc->xsize * 8;  // winv staging mirrors the x layout
+            wa = *reinterpret_cast<const double *>(sm + xb + pa);
+            wc = *reinterpret_cast<const double *>(sm + xb + pc);
+            we = *reinterpret_cast<const double *>(sm + xb + pe);
+        }
+        const double eps = cc->eps;
+        t0 = dykstra_row<UNIT>(p, c, e, wa, wc, we, y0, eps, viol);  // IJ: x_ij <= x_ik + x_jk
+        t1 = dykstra_row<UNIT>(c, p, e, wc, wa, we, y1, eps, viol);  // IK: x_ik <= x_ij + x_jk
+        t2 = dykstra_row<UNIT>(e, p, c, we, wa, wc, y2, eps, viol);  // JK: x_jk <= x_ij + x_ik
+        *xa = p;
+        *xc = c;
+        *xe = e;
+    }
+    wr_append(wd, cc->wp, cc->ctr, cc->T.stream0 + (tid >> 5), base, lane, t0, t1, t2);
+    return viol;
+}
+
 // ---------------------------------------------------------------------------
 // the tile kernel: one CTA = one tile of the round
 // ---------------------------------------------------------------------------
-// Largest CTA for S slots per thread (keeps >= 72 registers per thread).
-__host__ __device__ constexpr int max_threads_for(int S) { return S == 1 ? 1024 : (S == 2 ? 832 : 768); }
+// Shared-memory map (byte offsets from a 1024-aligned base):
+//   [0, b*W*8)            WR rows (1024 B each for W = 128)
+//   [b*W*8, 2*b*W*8)      WK rows
+//   [2*b*W*8, +W*8)       ZERO row (dummy target of inactive slots)
+//   then RK[b*b], then (general W) the same layout for 1/reg_x, then the
+//   per-warp dual state.
+// Ring rows are W*8-aligned, so a slot's ring address is one LOP3:
+// ((L - i - k) * 8 & (W*8 - 8)) | row_base.
+template <int W>
+struct SmemMap {
+    int b;
+    __device__ __host__ int wr() const { return 0; }
+    __device__ __host__ int wk() const { return b * W * 8; }
+    __device__ __host__ int zero() const { return 2 * b * W * 8; }
+    __device__ __host__ int rk() const { return 2 * b * W * 8 + W * 8; }
+    __device__ __host__ int xbytes() const { return rk() + ((b * b * 8 + W * 8 - 1) / (W * 8)) * W * 8; }
+};
+
+template <int S>
+struct SlotGeom {
+    int ik8[S];       // (i + k) * 8
+    int off[S];       // active iff (unsigned)(L - off) <= span
+    unsigned span[S];
+    int pik[S];       // byte offset of x_ik (RK) or of the zero row
+    int wr[S];        // byte offset of WR row ii (or zero row)
+    int wk[S];        // byte offset of WK row kk (or zero row)
+    int rkr[S];       // RK byte offset of x_ij when j in K:  rkr + 8j
+    int rkc[S];       // RK byte offset of x_jk when j in R:  8*b*j + rkc
+};
+
+__device__ __forceinline__ double lds64(const unsigned char *base, int off) {
+    return *reinterpret_cast<const double *>(base + off);
+}
+
+// acc | (d0 > 0 || d1 > 0 || d2 > 0), as three chained DSETPs
+__device__ __forceinline__ unsigned any_positive(double d0, double d1, double d2, unsigned acc) {
+    unsigned r;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.gt.f64 p, %1, 0d0000000000000000;\n\t"
+        "setp.gt.or.f64 p, %2, 0d0000000000000000, p;\n\t"
+        "setp.gt.or.f64 p, %3, 0d0000000000000000, p;\n\t"
+        "selp.u32 %0, 1, %4, p;\n\t}"
+        : "=r"(r)
+        : "d"(d0), "d"(d1), "d"(d2), "r"(acc));
+    return r;
+}
+
+// Hot part of one level: bit s set when slot s saw a violated row; the
+// slots' byte offsets are left in pa/pc/pe for the cold path.
+// Branch-free: inactive slots read the zero row (all row values 0).
+template <int S, int W, bool ALIAS>
+__device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const SlotGeom<S> &G, int L,
+                                              int b, int ihi, int klo, int (&pa)[S], int (&pc)[S],
+                                              int (&pe)[S]) {
+    const int L8 = L * 8;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int j8 = L8 - G.ik8[s];
+        const int jm = j8 & (W * 8 - 8);
+        if (ALIAS) {
+            const bool act = (unsigned)(L - G.off[s]) <= G.span[s];
+            const int j = j8 >> 3;
+            int a0 = j >= klo ? G.rkr[s] + j8 : (jm | G.wr[s]);
+            int e0 = j <= ihi ? j * (8 * b) + G.rkc[s] : (jm | G.wk[s]);
+            const int z = SmemMap<W>{b}.zero();
+            pa[s] = act ? a0 : z;
+            pe[s] = act ? e0 : z;
+            pc[s] = act ? G.pik[s] : z;
+        } else {
+            pa[s] = jm | G.wr[s];
+            pe[s] = jm | G.wk[s];
+            pc[s] = G.pik[s];
+        }
+    }
+    double xa[S], xc[S], xe[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        xa[s] = lds64(sm, pa[s]);
+        xc[s] = lds64(sm, pc[s]);
+        xe[s] = lds64(sm, pe[s]);
+    }
+    unsigned bits = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        // (c - a) == -(a - c) exactly in IEEE arithmetic
+        const double t = __dsub_rn(xa[s], xc[s]);
+        const double d0 = __dsub_rn(t, xe[s]);
+        const double d1 = __dsub_rn(-t, xe[s]);
+        const double d2 = __dsub_rn(__dsub_rn(xe[s], xa[s]), xc[s]);
+        bits |= any_positive(d0, d1, d2, 0u) << s;
+    }
+    return bits;
+}
+
+template <int S, int W, bool UNIT, bool ALIAS>
+__device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, double *smd,
+                                      const SlotGeom<S> &G, CtaConst &cc, RingState &rs,
+                                      WarpDuals *wd, int b, int ihi, int klo, int ring_end,
+                                      int &ring_L, uint32_t &head, double &viol) {
+    const TileDesc &T = cc.T;
+    uint32_t base0 = (uint32_t)(La - T.Lbeg) * (uint32_t)(S * 96);
+    const int dbg = cc.dbg;
+    for (int L = La; L <= Lb; ++L, base0 += (uint32_t)(S * 96)) {
+        if (!(dbg & 4) && L >= ring_L && L <= ring_end) ring_L = ring_step<W, UNIT>(smd, &cc, &rs, L);
+        int pa[S], pc[S], pe[S];
+        const unsigned bits = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe);
+        const unsigned wbits = __reduce_or_sync(0xffffffffu, bits);
+        // a violated row or a stored dual in this level: replay those slots exactly
+        if (!(dbg & 2) && (wbits != 0u || head < base0 + (uint32_t)(S * 96))) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t bs = base0 + (uint32_t)(s * 96);
+                if (((wbits >> s) & 1u) || head < bs + 96u) {
+                    viol = cold_slot<W, UNIT>(sm, &cc, wd, bs, pa[s], pc[s], pe[s], viol);
+                    head = wd->head;
+                }
+            }
+        }
+        if (!(dbg & 1)) __syncthreads();
+    }
+}
 
 template <int S, int W, bool UNIT>
-__global__ void __launch_bounds__(max_threads_for(S), 1) tile_round_kernel(TileArgs a) {
-    extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ CtaConst cc;
+    __shared__ RingState rs;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const TileDesc T = a.tiles[blockIdx.x];
-    const int b = a.b, nt = a.nt, tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
+    const int b = a.b, nt = a.nt;
     const int bb = b * b;
-    double *RK = smem;
-    double *WR = RK + bb;
-    double *WK = WR + b * W;
-    const int xsize = bb + 2 * b * W;  // doubles of x staging; winv staging follows
-    const double eps = a.eps;
+    const SmemMap<W> M{b};
+    // 1024-aligned base (the launch reserves 1 KiB of slack)
+    unsigned char *sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    double *smd = reinterpret_cast<double *>(sm);
+    const int xb = M.xbytes();
+    WarpDuals *wds = reinterpret_cast<WarpDuals *>(sm + xb * (UNIT ? 1 : 2));
+    WarpDuals *wd = wds + warp;
+    double *WR = smd + M.wr() / 8;
+    double *WK = smd + M.wk() / 8;
+    double *RK = smd + M.rk() / 8;
+    const int xsize = xb / 8;  // doubles between x staging and winv staging
+    if (tid == 0) {
+        cc.T = T;
+        cc.x = a.x;
+        cc.winvx = a.winvx;
+        cc.ld = a.ld;
+        cc.eps = a.eps;
+        cc.rp = a.rp;
+        cc.wp = a.wp;
+        cc.ctr = a.ctr;
+        cc.b = b;
+        cc.nt = nt;
+        cc.xsize = xsize;
+        cc.dbg = a.dbg;
+    }
+    for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
 
     // --- per-slot geometry --------------------------------------------------
-    int off[S];      // level L is active for the slot iff (unsigned)(L-off) <= span
-    unsigned span[S];
-    int si[S], sk[S];  // i - ilo, k - klo
+    // Slot s of this thread owns the pair (i,k) = (ilo + q/b, klo + q%b),
+    // q = tid + s*nt; at level L it processes j = L - (i+k).
+    SlotGeom<S> G;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const int q = tid + s * nt;
@@ -383,10 +709,14 @@ __global__ void __launch_bounds__(max_threads_for(S), 1) tile_round_kernel(TileA
         const int i = T.ilo + ii, k = T.klo + kk;
         const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
         const bool ok = q < bb && i <= T.ihi && k <= T.z && js <= je;
-        si[s] = ii;
-        sk[s] = kk;
-        off[s] = ok ? i + k + js : 0x3fffffff;
-        span[s] = ok ? (unsigned)(je - js) : 0u;
+        G.ik8[s] = ok ? 8 * (i + k) : 0;
+        G.off[s] = ok ? i + k + js : 0x3fffffff;
+        G.span[s] = ok ? (unsigned)(je - js) : 0u;
+        G.pik[s] = ok ? M.rk() + 8 * (ii * b + kk) : M.zero();
+        G.wr[s] = ok ? M.wr() + ii * W * 8 : M.zero();
+        G.wk[s] = ok ? M.wk() + kk * W * 8 : M.zero();
+        G.rkr[s] = ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero();
+        G.rkc[s] = ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero();
     }
 
     // --- staging prologue ---------------------------------------------------
@@ -396,108 +726,63 @@ __global__ void __launch_bounds__(max_threads_for(S), 1) tile_round_kernel(TileA
     rk_block<true>(T, b, a.ld, a.x, RK, tid, nt);
     if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt);
     const int blast = T.jhi / BLK;
-    int lo_res = max(T.Lbeg - T.ihi - T.z, T.jlo) / BLK;  // lowest block not written back
-    int hi_issued = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
-    for (int bk = lo_res; bk <= hi_issued; ++bk) {
+    const int lo0 = max(T.Lbeg - T.ihi - T.z, T.jlo) / BLK;
+    const int hi0 = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
+    for (int bk = lo0; bk <= hi0; ++bk) {
         ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
         if (!UNIT)
             ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
                                 bk, tid, nt);
     }
     cp_async_commit();
+    if (tid == 0) {
+        rs.lo_res = lo0;
+        rs.hi_issued = hi0;
+        rs.hi_landed = hi0;
+        rs.blast = blast;
+    }
+    // --- dual streams --------------------------------------------------------
+    rd_init(wd, a.rp, T.stream0 + warp, lane);
     cp_async_wait_all();
     __syncthreads();
-    int hi_landed = hi_issued;
-
-    // --- dual streams --------------------------------------------------------
-    const int64_t stream = T.stream0 + warp;
-    StreamReader rd;
-    rd.init(a.rp, stream, lane);
-    StreamWriter wr;
-    wr.init();
 
     double viol = 0.0;
-    const int ihi = T.ihi, klo = T.klo, ilo = T.ilo;
-
-    for (int L = T.Lbeg; L <= T.Lend; ++L) {
-        const int need_hi = min(L - ilo - klo, T.jhi) / BLK;
-        if (need_hi > hi_landed) {  // uniform: the wavefront top enters a new block
-            const int low_need = max(L - ihi - T.z, T.jlo) / BLK;
-            for (; lo_res < low_need; ++lo_res)
-                ring_block<W, false>(T, b, a.ld, a.x, WR, WK, lo_res, tid, nt);
-            // catch up if the block needed now was never prefetched
-            for (; hi_issued < need_hi;) {
-                ++hi_issued;
-                ring_block<W, true>(T, b, a.ld, a.x, WR, WK, hi_issued, tid, nt);
-                if (!UNIT)
-                    ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize,
-                                        WK + xsize, hi_issued, tid, nt);
-                cp_async_commit();
-            }
-            cp_async_wait_all();
-            __syncthreads();  // landed data visible; write-back reads done
-            hi_landed = hi_issued;
-            if (hi_issued < blast) {  // prefetch one block ahead of the wavefront
-                ++hi_issued;
-                ring_block<W, true>(T, b, a.ld, a.x, WR, WK, hi_issued, tid, nt);
-                if (!UNIT)
-                    ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize,
-                                        WK + xsize, hi_issued, tid, nt);
-                cp_async_commit();
-            }
-        }
-
-        const uint32_t lbase = (uint32_t)(L - T.Lbeg) * (uint32_t)S;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const uint32_t base = (lbase + (uint32_t)s) * 96u;
-            double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-            rd.lookup(a.rp, base, lane, y0, y1, y2);
-            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-            if ((unsigned)(L - off[s]) <= span[s]) {
-                const int i = ilo + si[s], k = klo + sk[s];
-                const int j = L - i - k;
-                const int pij = j >= klo ? si[s] * b + (j - klo) : bb + si[s] * W + (j & (W - 1));
-                const int pjk = j <= ihi ? (j - ilo) * b + sk[s]
-                                         : bb + b * W + sk[s] * W + (j & (W - 1));
-                const int pik = si[s] * b + sk[s];
-                double xa = smem[pij], xc = smem[pik], xe = smem[pjk];
-                const double d0 = __dsub_rn(__dsub_rn(xa, xc), xe);
-                const double d1 = __dsub_rn(__dsub_rn(xc, xa), xe);
-                const double d2 = __dsub_rn(__dsub_rn(xe, xa), xc);
-                const bool slow = (y0 != 0.0) | (y1 != 0.0) | (y2 != 0.0) | (d0 > 0.0) |
-                                  (d1 > 0.0) | (d2 > 0.0);
-                if (slow) {
-                    if (UNIT) {
-                        t0 = dykstra_row_unit(xa, xc, xe, y0, eps, viol);  // IJ: x_ij <= x_ik + x_jk
-                        t1 = dykstra_row_unit(xc, xa, xe, y1, eps, viol);  // IK: x_ik <= x_ij + x_jk
-                        t2 = dykstra_row_unit(xe, xa, xc, y2, eps, viol);  // JK: x_jk <= x_ij + x_ik
-                    } else {
-                        const double wa = smem[xsize + pij], wc = smem[xsize + pik],
-                                     we = smem[xsize + pjk];
-                        t0 = dykstra_row(xa, xc, xe, wa, wc, we, y0, eps, viol);
-                        t1 = dykstra_row(xc, xa, xe, wc, wa, we, y1, eps, viol);
-                        t2 = dykstra_row(xe, xa, xc, we, wa, wc, y2, eps, viol);
-                    }
-                    smem[pij] = xa;
-                    smem[pik] = xc;
-                    smem[pjk] = xe;
-                }
-            }
-            wr.append(a.wp, a.ctr, stream, base, lane, t0, t1, t2);
-        }
-        __syncthreads();
+    const int ihi = T.ihi, klo = T.klo;
+    // the top j = L - ilo - klo leaves the landed blocks at ring_L
+    int ring_L = BLK * (hi0 + 1) + T.ilo + T.klo;
+    const int ring_end = T.jhi + T.ilo + T.klo;  // top j past jhi: nothing more to land
+    uint32_t head = wd->head;
+    // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or K)
+    // iff L in (2*ihi + z, 2*klo + ilo).
+    const int mid_a = max(2 * ihi + T.z + 1, T.Lbeg);
+    const int mid_b = min(2 * klo + T.ilo - 1, T.Lend);
+    if (mid_a <= mid_b) {
+        sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
+                                ring_L, head, viol);
+        sweep<S, W, UNIT, false>(mid_a, mid_b, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
+                                 ring_L, head, viol);
+        sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
+                                ring_L, head, viol);
+    } else {
+        sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
+                                ring_L, head, viol);
     }
 
     // --- epilogue: write back everything still staged ------------------------
     cp_async_wait_all();
     __syncthreads();
-    for (; lo_res <= hi_issued; ++lo_res)
-        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, lo_res, tid, nt);
+    for (int bk = rs.lo_res; bk <= rs.hi_issued; ++bk)
+        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
     rk_block<false>(T, b, a.ld, a.x, RK, tid, nt);
-    wr.finish(a.wp, stream, lane);
+    wr_finish(wd, a.wp, a.ctr, T.stream0 + warp, lane);
     viol = warp_max(viol);
     if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
+}
+
+// dynamic shared memory of one CTA (+1 KiB alignment slack)
+inline size_t tile_smem_bytes(int b, int W, bool unit, int nt) {
+    const size_t xb = W == 64 ? SmemMap<64>{b}.xbytes() : SmemMap<128>{b}.xbytes();
+    return 1024 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
 }
 
 }  // namespace mp

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -128,9 +129,7 @@ struct mp_handle {
         for (double *p : bufs)
             if (p) cudaFree(p);
         for (auto &p : pool) {
-            cudaFree(p.keys);
-            cudaFree(p.vals);
-            cudaFree(p.next);
+            cudaFree(p.rec);
             cudaFree(p.head);
         }
         cudaFree(d_tiles);
@@ -149,15 +148,9 @@ namespace {
 
 int alloc_pool(mp_handle *h, int which, int32_t cap) {
     DualPool &p = h->pool[which];
-    cudaFree(p.keys);
-    cudaFree(p.vals);
-    cudaFree(p.next);
-    p.keys = nullptr;
-    p.vals = nullptr;
-    p.next = nullptr;
-    CK(cudaMalloc(&p.keys, (size_t)cap * CHUNK * sizeof(uint32_t)));
-    CK(cudaMalloc(&p.vals, (size_t)cap * CHUNK * sizeof(double)));
-    CK(cudaMalloc(&p.next, (size_t)cap * sizeof(int32_t)));
+    cudaFree(p.rec);
+    p.rec = nullptr;
+    CK(cudaMalloc(&p.rec, (size_t)cap * sizeof(ChunkRec)));
     p.cap = cap;
     if (!p.head) {
         CK(cudaMalloc(&p.head, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
@@ -189,7 +182,9 @@ int launch_tiles(mp_handle *h, const TileArgs &a, int ntiles) {
     switch (h->S) {
         case 1: return launch_tiles_s<1>(h, a, ntiles);
         case 2: return launch_tiles_s<2>(h, a, ntiles);
-        default: return launch_tiles_s<3>(h, a, ntiles);
+        case 3: return launch_tiles_s<3>(h, a, ntiles);
+        case 4: return launch_tiles_s<4>(h, a, ntiles);
+        default: return launch_tiles_s<5>(h, a, ntiles);
     }
 }
 
@@ -227,6 +222,7 @@ int enqueue_pass(mp_handle *h) {
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[wp];
     ta.ctr = h->ctr;
+    ta.dbg = getenv("MP_DBG") ? atoi(getenv("MP_DBG")) : 0;
     for (size_t r = 0; r < h->round_cnt.size(); ++r) {
         if (!h->round_cnt[r]) continue;
         ta.tiles = h->d_tiles + h->round_off[r];
@@ -369,9 +365,13 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         }
 
     // ---- schedule (schedule.tiled_rounds, schedule.py:117-153) -------------
-    for (h->S = 1;; ++h->S) {
+    {
+        // threads per CTA: env MP_CTA_THREADS (tuning), default 512
+        int target = MAX_CTA_THREADS;
+        if (const char *e = getenv("MP_CTA_THREADS")) target = std::max(32, std::min(MAX_CTA_THREADS, atoi(e)));
+        h->S = std::min((b * b + target - 1) / target, MAX_SLOTS);
         h->NT = ((b * b + h->S - 1) / h->S + 31) / 32 * 32;
-        if (h->NT <= max_threads_for(h->S)) break;
+        if (h->NT > MAX_CTA_THREADS) return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d needs too many threads", b));
     }
     h->W = b <= 16 ? 64 : 128;
     const int nwarps = h->NT / 32;
@@ -400,8 +400,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         const uint64_t keys = (uint64_t)(t.Lend - t.Lbeg + 1) * (uint64_t)h->S * 96ull;
         if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
     }
-    const size_t xsz = (size_t)b * b + 2 * (size_t)b * h->W;
-    h->smem = xsz * sizeof(double) * (h->unit_x ? 1 : 2);
+    h->smem = tile_smem_bytes(b, h->W, h->unit_x, h->NT);
     if (h->smem > 227 * 1024) return bail(fail(MP_ERR_UNSUPPORTED, "tile staging needs %zu bytes of shared memory", h->smem));
 
     int rc;
@@ -489,7 +488,7 @@ int mp_run_passes(mp_handle *h, int32_t npasses, mp_pass_stats *out) {
         const int64_t want = std::max<int64_t>(h->pool[wp].cap, 2 * (int64_t)h->pool_used[h->rp] + 1024);
         if (want > h->pool[wp].cap) {
             CK(cudaStreamSynchronize(h->st));
-            int rc = alloc_pool(h, wp, (int32_t)std::min<int64_t>(want, 0x7fffffff / CHUNK));
+            int rc = alloc_pool(h, wp, (int32_t)std::min<int64_t>(want, 0x7fffffff));
             if (rc) return rc;
         }
         for (int attempt = 0;; ++attempt) {
@@ -504,7 +503,7 @@ int mp_run_passes(mp_handle *h, int32_t npasses, mp_pass_stats *out) {
             CK(cudaStreamSynchronize(h->st));
             const int64_t grow = std::max<int64_t>(2 * (int64_t)h->pool[wp].cap,
                                                    (int64_t)h->h_stats->chunks_used * 2);
-            if (attempt > 8 || grow > 0x7fffffff / CHUNK)
+            if (attempt > 8 || grow > 0x7fffffff)
                 return fail(MP_ERR_OOM, "dual pool cannot grow further");
             rc = alloc_pool(h, wp, (int32_t)grow);
             if (rc) return rc;
@@ -588,14 +587,10 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
     if (!keys && !vals) return MP_OK;
     const DualPool &P = h->pool[h->rp];
     const int64_t used = h->pool_used[h->rp];
-    std::vector<uint32_t> hk((size_t)used * CHUNK);
-    std::vector<double> hv((size_t)used * CHUNK);
-    std::vector<int32_t> hn((size_t)used), hh((size_t)h->nstreams);
-    if (used) {
-        CK(cudaMemcpyAsync(hk.data(), P.keys, hk.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaMemcpyAsync(hv.data(), P.vals, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaMemcpyAsync(hn.data(), P.next, hn.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
-    }
+    std::vector<ChunkRec> hr((size_t)used);
+    std::vector<int32_t> hh((size_t)h->nstreams);
+    if (used)
+        CK(cudaMemcpyAsync(hr.data(), P.rec, hr.size() * sizeof(ChunkRec), cudaMemcpyDeviceToHost, h->st));
     if (h->nstreams)
         CK(cudaMemcpyAsync(hh.data(), P.head, hh.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
@@ -615,7 +610,7 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
             int32_t c = used ? hh[(size_t)(h->tiles[t].stream0 + w)] : -1;
             while (c >= 0 && c < used) {
                 for (int e = 0; e < CHUNK; ++e) {
-                    const uint32_t key = hk[(size_t)c * CHUNK + e];
+                    const uint32_t key = hr[(size_t)c].keys[e];
                     if (key == KEY_END) break;
                     Decoded dd = decode_entry(h, (int64_t)t, w, key);
                     E en;
@@ -626,10 +621,10 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
                     en.rank[3] = dd.i;
                     en.rank[4] = dd.kind;
                     en.key = ((dd.i * n + dd.j) * n + dd.k) * 3 + dd.kind;
-                    en.val = hv[(size_t)c * CHUNK + e];
+                    en.val = hr[(size_t)c].vals[e];
                     ents.push_back(en);
                 }
-                c = hn[(size_t)c];
+                c = hr[(size_t)c].next;
             }
         }
         std::sort(ents.begin(), ents.end(), [](const E &a, const E &b) {
@@ -682,10 +677,9 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
     for (size_t e = 1; e < ents.size(); ++e)
         if (ents[e].first == ents[e - 1].first && ents[e].second.first == ents[e - 1].second.first)
             return fail(MP_ERR_ARG, "duplicate dual key");
-    // pack into chunks
-    std::vector<uint32_t> hk;
-    std::vector<double> hv;
-    std::vector<int32_t> hn, hh((size_t)h->nstreams, -1);
+    // pack into chunk records
+    std::vector<ChunkRec> hr;
+    std::vector<int32_t> hh((size_t)h->nstreams, -1);
     size_t e = 0;
     while (e < ents.size()) {
         const int64_t s = ents[e].first;
@@ -693,34 +687,34 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         size_t cnt = 0;
         while (e < ents.size() && ents[e].first == s) {
             if (cnt % CHUNK == 0) {
-                const int32_t c = (int32_t)hn.size();
-                hn.push_back(-1);
-                hk.resize(hk.size() + CHUNK, KEY_END);
-                hv.resize(hv.size() + CHUNK, 0.0);
-                if (prev >= 0) hn[(size_t)prev] = c;
+                const int32_t c = (int32_t)hr.size();
+                ChunkRec r;
+                std::memset(&r, 0, sizeof(r));
+                for (int q = 0; q < CHUNK; ++q) r.keys[q] = KEY_END;
+                r.next = -1;
+                hr.push_back(r);
+                if (prev >= 0) hr[(size_t)prev].next = c;
                 else hh[(size_t)s] = c;
                 prev = c;
             }
-            hk[(size_t)prev * CHUNK + cnt % CHUNK] = ents[e].second.first;
-            hv[(size_t)prev * CHUNK + cnt % CHUNK] = ents[e].second.second;
+            hr[(size_t)prev].keys[cnt % CHUNK] = ents[e].second.first;
+            hr[(size_t)prev].vals[cnt % CHUNK] = ents[e].second.second;
             ++cnt;
             ++e;
         }
     }
-    const int32_t used = (int32_t)hn.size();
+    const int32_t used = (int32_t)hr.size();
     const int rp = h->rp;
     if (used > h->pool[rp].cap) {
         int rc = alloc_pool(h, rp, std::max<int32_t>(used * 2, 4096));
         if (rc) return rc;
     }
     DualPool &P = h->pool[rp];
-    if (used) {
-        CK(cudaMemcpyAsync(P.keys, hk.data(), hk.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(P.vals, hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(P.next, hn.data(), hn.size() * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
-    }
+    if (used)
+        CK(cudaMemcpyAsync(P.rec, hr.data(), hr.size() * sizeof(ChunkRec), cudaMemcpyHostToDevice, h->st));
     if (h->nstreams)
         CK(cudaMemcpyAsync(P.head, hh.data(), hh.size() * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
     h->pool_used[rp] = used;
     h->nnz = nnz;
     if (pair_duals) {

@@ -245,3 +245,65 @@ def critical_levels(n, b):
         if rnd.units:
             total += max(hi - lo + 1 for lo, hi in (t.levels() for t in rnd.units))
     return total
+
+
+# ---------------------------------------------------------------------------
+# algorithmic traffic
+# ---------------------------------------------------------------------------
+
+def _tile_arrays(n, b):
+    xs, zs = [], []
+    for x0, z0 in [(1 - b, z) for z in range(n - 1, 1, -b)] + [(x, n - 1) for x in range(1, n - 2, b)]:
+        c = 0
+        while max(x0 + c * b, 0) + 2 <= z0 - c * b:
+            xs.append(x0 + c * b)
+            zs.append(z0 - c * b)
+            c += 1
+    import numpy as np
+    return np.array(xs, dtype=np.int64), np.array(zs, dtype=np.int64)
+
+
+def touched_pairs(n, b, chunk=2048):
+    """T_x(n, b): sum over all tiles of a pass of the distinct pairs the tile
+    touches (R x J, J x K, R x K with i < j < k), i.e. the pairs one pass
+    must read and write once each under the tiled schedule."""
+    import numpy as np
+    X, Z = _tile_arrays(n, b)
+    total = 0
+    ar = np.arange(b, dtype=np.int64)
+    for s in range(0, len(X), chunk):
+        x, z = X[s:s + chunk, None], Z[s:s + chunk, None]
+        ilo, ihi = np.maximum(x, 0), x + b - 1
+        klo = np.maximum(z - b + 1, 0)
+        jlo, jhi = np.maximum(x + 1, 1), z - 1
+        i = ilo + ar[None, :]                       # (T, b) rows
+        k = klo + ar[None, :]                       # (T, b) cols
+        iv = (i <= ihi) & (i <= n - 1)
+        kv = k <= z
+        # R x J with j outside K (j < klo)
+        wr = np.clip(np.minimum(jhi, klo - 1) - np.maximum(jlo, i + 1) + 1, 0, None)
+        total += int((wr * iv).sum())
+        # J x K with j outside R (j > ihi)
+        wk = np.clip(np.minimum(jhi, k - 1) - np.maximum(jlo, ihi + 1) + 1, 0, None)
+        total += int((wk * kv).sum())
+        # R x K pairs touched in any role
+        I, K = i[:, :, None], k[:, None, :]
+        JLO, JHI, ILO = jlo[:, :, None], jhi[:, :, None], ilo[:, :, None]
+        valid = iv[:, :, None] & kv[:, None, :] & (I < K)
+        as_ik = np.maximum(I + 1, JLO) <= np.minimum(K - 1, JHI)
+        as_ij = (K >= JLO) & (K <= JHI)
+        as_jk = (I >= JLO) & (I <= JHI) & (I > ILO)
+        total += int((valid & (as_ik | as_ij | as_jk)).sum())
+    return total
+
+
+def touched_pairs_brute(n, b):
+    """Reference count by enumeration (small n only)."""
+    total = 0
+    for rnd in tiled_rounds(n, b):
+        for t in rnd.units:
+            s = set()
+            for (i, j, k) in tile_triplets(t, n):
+                s.update(((i, j), (i, k), (j, k)))
+            total += len(s)
+    return total
