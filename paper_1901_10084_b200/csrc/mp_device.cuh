@@ -574,16 +574,25 @@ __device__ __forceinline__ double lds64(const unsigned char *base, int off) {
     return *reinterpret_cast<const double *>(base + off);
 }
 
-// acc | (d0 > 0 || d1 > 0 || d2 > 0), as three chained DSETPs
-__device__ __forceinline__ unsigned any_positive(double d0, double d1, double d2, unsigned acc) {
+// Violation test of one triplet without forming the three row values.
+// For finite or infinite x, y: fl(x - y) > 0  <=>  x > y (round-to-nearest
+// keeps the sign and gradual underflow never rounds a nonzero difference to
+// 0; NaN compares false both ways).  With t = fl(a - c), fl(c - a) = -t, so
+//   d0 = fl(t - e) > 0   <=>  t > e
+//   d1 = fl(-t - e) > 0  <=>  -t > e        i.e. (d0 > 0 || d1 > 0) <=> |t| > e
+//   d2 = fl(fl(e - a) - c) > 0  <=>  fl(e - a) > c
+// Two DADDs and two DSETPs instead of five and three; returns 1 if violated.
+__device__ __forceinline__ unsigned triplet_violated(double a, double c, double e) {
     unsigned r;
-    asm("{\n\t.reg .pred p;\n\t"
-        "setp.gt.f64 p, %1, 0d0000000000000000;\n\t"
-        "setp.gt.or.f64 p, %2, 0d0000000000000000, p;\n\t"
-        "setp.gt.or.f64 p, %3, 0d0000000000000000, p;\n\t"
-        "selp.u32 %0, 1, %4, p;\n\t}"
+    asm("{\n\t.reg .pred p;\n\t.reg .f64 t, u;\n\t"
+        "sub.rn.f64 t, %1, %2;\n\t"
+        "sub.rn.f64 u, %3, %1;\n\t"
+        "abs.f64 t, t;\n\t"
+        "setp.gt.f64 p, t, %3;\n\t"
+        "setp.gt.or.f64 p, u, %2, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(r)
-        : "d"(d0), "d"(d1), "d"(d2), "r"(acc));
+        : "d"(a), "d"(c), "d"(e));
     return r;
 }
 
@@ -593,7 +602,7 @@ __device__ __forceinline__ unsigned any_positive(double d0, double d1, double d2
 template <int S, int W, bool ALIAS>
 __device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const SlotGeom<S> &G, int L,
                                               int b, int ihi, int klo, int (&pa)[S], int (&pc)[S],
-                                              int (&pe)[S]) {
+                                              int (&pe)[S], const double (&xcr)[S]) {
     const int L8 = L * 8;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -618,19 +627,13 @@ __device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const Slo
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         xa[s] = lds64(sm, pa[s]);
-        xc[s] = lds64(sm, pc[s]);
+        // alias-free levels: x_ik belongs to this thread alone, kept in a register
+        xc[s] = ALIAS ? lds64(sm, pc[s]) : xcr[s];
         xe[s] = lds64(sm, pe[s]);
     }
     unsigned bits = 0;
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-        // (c - a) == -(a - c) exactly in IEEE arithmetic
-        const double t = __dsub_rn(xa[s], xc[s]);
-        const double d0 = __dsub_rn(t, xe[s]);
-        const double d1 = __dsub_rn(-t, xe[s]);
-        const double d2 = __dsub_rn(__dsub_rn(xe[s], xa[s]), xc[s]);
-        bits |= any_positive(d0, d1, d2, 0u) << s;
-    }
+    for (int s = 0; s < S; ++s) bits |= triplet_violated(xa[s], xc[s], xe[s]) << s;
     return bits;
 }
 
@@ -642,10 +645,13 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, double 
     const TileDesc &T = cc.T;
     uint32_t base0 = (uint32_t)(La - T.Lbeg) * (uint32_t)(S * 96);
     const int dbg = cc.dbg;
+    double xcr[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) xcr[s] = ALIAS ? 0.0 : lds64(sm, G.pik[s]);
     for (int L = La; L <= Lb; ++L, base0 += (uint32_t)(S * 96)) {
         if (!(dbg & 4) && L >= ring_L && L <= ring_end) ring_L = ring_step<W, UNIT>(smd, &cc, &rs, L);
         int pa[S], pc[S], pe[S];
-        const unsigned bits = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe);
+        const unsigned bits = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
         const unsigned wbits = __reduce_or_sync(0xffffffffu, bits);
         // a violated row or a stored dual in this level: replay those slots exactly
         if (!(dbg & 2) && (wbits != 0u || head < base0 + (uint32_t)(S * 96))) {
@@ -655,6 +661,7 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, double 
                 if (((wbits >> s) & 1u) || head < bs + 96u) {
                     viol = cold_slot<W, UNIT>(sm, &cc, wd, bs, pa[s], pc[s], pe[s], viol);
                     head = wd->head;
+                    if (!ALIAS) xcr[s] = lds64(sm, pc[s]);  // the exact step may move x_ik
                 }
             }
         }
