@@ -125,6 +125,11 @@ int mp_state_max_violation(mp_handle *h, double *out);
  * session was created with MP_FLAG_TIME_ROUNDS; launches = kernels launched. */
 int mp_get_timing(mp_handle *h, double *metric_ms, double *pair_ms, int64_t *launches);
 
+/* Optional in-kernel cycle counters of the tile kernel (diagnostics):
+ * enable != 0 turns them on for later passes; out (if non-NULL) receives up
+ * to nslots counters accumulated since the last read and resets them. */
+int mp_trace(mp_handle *h, int32_t enable, uint64_t *out, int32_t nslots);
+
 /* Write a buffer larger than L2 on the session's stream (benchmark hygiene). */
 int mp_flush_l2(mp_handle *h);
 

@@ -41,24 +41,27 @@ def sources():
                   if f.endswith((".cu", ".cuh", ".h", ".cpp")))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/ into _lib/libmetricproj_b200.so (sm_100a)."""
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Compile csrc/ into _lib/libmetricproj_b200.so (sm_100a).  A named
+    ``variant`` with extra ``defines`` (e.g. MP_TRACE) builds a side library
+    for diagnostics, selected at load time with MP_LIB_VARIANT."""
     os.makedirs(LIB_DIR, exist_ok=True)
+    out = LIB_PATH if not variant else os.path.join(LIB_DIR, f"libmetricproj_b200_{variant}.so")
     deps = sources() + [os.path.join(INCLUDE, "metricproj_b200.h")]
-    if (not force and os.path.exists(LIB_PATH)
-            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(p) for p in deps)):
-        return LIB_PATH
+    if (not force and os.path.exists(out)
+            and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in deps)):
+        return out
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC,
+    tmp = out + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-I", CSRC,
            "-o", tmp, os.path.join(CSRC, "mp_solver.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, out)
+    return out
 
 
 class MPInstance(ctypes.Structure):
@@ -91,7 +94,7 @@ class MPPassStats(ctypes.Structure):
 # every symbol include/metricproj_b200.h declares
 EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dual_count",
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
-           "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_last_error", "mp_version")
+           "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_last_error", "mp_version")
 
 _lib = None
 
@@ -101,11 +104,13 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    variant = os.environ.get("MP_LIB_VARIANT", "")
+    path = LIB_PATH if not variant else os.path.join(LIB_DIR, f"libmetricproj_b200_{variant}.so")
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is missing: run paper_1901_10084_b200._native.build() "
+            f"{path} is missing: run paper_1901_10084_b200._native.build() "
             "(or __graft_entry__.build()); there is no CPU fallback")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     P = ctypes.c_void_p
     D = ctypes.POINTER(ctypes.c_double)
     I = ctypes.POINTER(ctypes.c_int64)
@@ -121,6 +126,8 @@ def load():
     L.mp_state_max_violation.argtypes = [P, D]
     L.mp_get_timing.argtypes = [P, D, D, I]
     L.mp_flush_l2.argtypes = [P]
+    L.mp_trace.argtypes = [P, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int32]
+    L.mp_trace.restype = ctypes.c_int
     L.mp_destroy.restype = None
     L.mp_destroy.argtypes = [P]
     L.mp_max_violation.argtypes = [ctypes.c_int64, D, D, D, D]

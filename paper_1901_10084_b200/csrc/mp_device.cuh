@@ -107,6 +107,14 @@ struct TileArgs {
     DualPool rp, wp;
     PassCounters *ctr;
     int32_t dbg;  // TEMP experiment switches
+    int32_t nwc;  // compute warps per CTA (the rest are ring producers)
+    unsigned long long *trace;  // optional cycle counters (mp_trace), null = off
+};
+
+// trace slots (cycles summed over warps / CTAs; see tools/trace_pass.py)
+enum TraceSlot {
+    TR_PRED_WAIT = 0, TR_RING_WAIT, TR_HOT, TR_COLD, TR_RELEASE, TR_LEVELS, TR_COLD_CALLS,
+    TR_PROLOGUE = 8, TR_LOOP, TR_EPILOGUE, TR_PROD_BUSY, TR_CTAS, TR_NSLOTS = 16
 };
 
 // Per-warp dual-stream state, in shared memory.
@@ -131,6 +139,7 @@ struct CtaConst {
     double eps;
     DualPool rp, wp;
     PassCounters *ctr;
+    unsigned long long *trace;
     int32_t b, nt, xsize, dbg;
 };
 
@@ -191,6 +200,7 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_2() { asm volatile("cp.async.wait_group 2;\n" ::); }
 
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -446,57 +456,6 @@ __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, d
     }
 }
 
-// Ring bookkeeping (CTA-uniform), kept in shared memory.
-struct RingState {
-    int32_t lo_res;     // lowest block not yet written back
-    int32_t hi_issued;  // highest block whose copy was issued
-    int32_t hi_landed;  // highest block known landed
-    int32_t blast;      // last block of J
-};
-
-// Called by the whole CTA when the wavefront top enters a block that has not
-// landed: write back passed blocks, land the needed one, prefetch the next.
-// Returns the level at which this must run again.
-template <int W, bool UNIT>
-__device__ __noinline__ int ring_step(double *smem, const CtaConst *cc, RingState *rs, int L) {
-    const TileDesc &T = cc->T;
-    const int b = cc->b, nt = cc->nt, tid = threadIdx.x, xsize = cc->xsize;
-    double *WR = smem, *WK = smem + b * W;  // SmemMap layout
-    const int need_hi = min(L - T.ilo - T.klo, T.jhi) / BLK;
-    const int low_need = max(L - T.ihi - T.z, T.jlo) / BLK;
-    int lo_res = rs->lo_res, hi_issued = rs->hi_issued;
-    const int blast = rs->blast;
-    for (; lo_res < low_need; ++lo_res)
-        ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, tid, nt);
-    for (; hi_issued < need_hi;) {  // catch up if the needed block was never prefetched
-        ++hi_issued;
-        ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, tid, nt);
-        if (!UNIT)
-            ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
-                                WK + xsize, hi_issued, tid, nt);
-        cp_async_commit();
-    }
-    cp_async_wait_all();
-    __syncthreads();  // landed data visible; write-back reads done; rs read by all
-    const int hi_landed = hi_issued;
-    if (hi_issued < blast) {  // prefetch one block ahead of the wavefront
-        ++hi_issued;
-        ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, tid, nt);
-        if (!UNIT)
-            ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
-                                WK + xsize, hi_issued, tid, nt);
-        cp_async_commit();
-    }
-    __syncthreads();  // everyone has read rs
-    if (tid == 0) {
-        rs->lo_res = lo_res;
-        rs->hi_issued = hi_issued;
-        rs->hi_landed = hi_landed;
-    }
-    // next time the top j = L - ilo - klo leaves block hi_landed
-    return BLK * (hi_landed + 1) + T.ilo + T.klo;
-}
-
 // ---------------------------------------------------------------------------
 // cold path: a warp replays one slot of one level with the full step
 // ---------------------------------------------------------------------------
@@ -637,24 +596,89 @@ __device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const Slo
     return bits;
 }
 
+// ---------------------------------------------------------------------------
+// warp-level dataflow
+// ---------------------------------------------------------------------------
+// Every conflict inside a tile is ordered along the (i,k) lattice: thread
+// (i,k) may run level L once (i,k-1) and (i-1,k) have finished level L-1
+// (this covers the aliased cross-role cases too: for any two conflicting
+// triplets, the later one's (i,k) is reachable from the earlier one's by
+// +1 steps in i or k, one level per step).  With the slot map
+// q = warp*32*S + s*32 + lane (q = (i-ilo)*b + (k-klo), b <= 32*S), both
+// neighbours of a warp's pairs live in the same warp or in warp-1, so a
+// compute warp only waits for its predecessor's progress counter -- no CTA
+// barrier per level, and a warp in the exact (cold) step delays only its
+// successors.  A producer warp streams the j-rings: it lands blocks ahead of
+// warp 0 and writes back blocks the last warp has passed.
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// Progress store of a level that wrote nothing: the level's shared loads
+// were consumed before this store issues, so no fence is needed for WAR.
+__device__ __forceinline__ void st_relaxed(int *p, int v) {
+    asm volatile("st.relaxed.cta.shared.b32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// spin until *p >= v (acquire), backing off so spinners do not steal issue slots
+__device__ __forceinline__ void wait_geq(const int *p, int v, bool sleep) {
+    if (ld_acquire(p) >= v) return;
+    while (true) {
+        if (sleep) __nanosleep(20);
+        if (ld_acquire(p) >= v) return;
+    }
+}
+
+struct TileSync {
+    int done[32];    // last level each compute warp finished
+    int landed;      // highest ring block landed
+    int lo_res;      // producer's lowest resident block (for the epilogue)
+    int hi_issued;   // producer's highest issued block (for the epilogue)
+    int pslow, pfast;  // producer-internal broadcast
+};
+
 template <int S, int W, bool UNIT, bool ALIAS>
-__device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, double *smd,
-                                      const SlotGeom<S> &G, CtaConst &cc, RingState &rs,
-                                      WarpDuals *wd, int b, int ihi, int klo, int ring_end,
-                                      int &ring_L, uint32_t &head, double &viol) {
+__device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const SlotGeom<S> &G,
+                                      CtaConst &cc, TileSync &ts, WarpDuals *wd, int warp, int b,
+                                      int ihi, int klo, uint32_t &head, double &viol) {
+    if (La > Lb) return;
     const TileDesc &T = cc.T;
+    const int lane = threadIdx.x & 31;
     uint32_t base0 = (uint32_t)(La - T.Lbeg) * (uint32_t)(S * 96);
-    const int dbg = cc.dbg;
     double xcr[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) xcr[s] = ALIAS ? 0.0 : lds64(sm, G.pik[s]);
+    bool xcr_valid = false;
+    const int dbg = cc.dbg;  // TEMP experiment switches
+#ifdef MP_TRACE
+    const bool tr = cc.trace != nullptr;
+#else
+    constexpr bool tr = false;  // build with -DMP_TRACE for mp_trace counters
+#endif
+    unsigned long long c_pred = 0, c_ring = 0, c_hot = 0, c_cold = 0, c_rel = 0, n_cold = 0;
+    long long t0 = tr ? clock64() : 0, t1;
     for (int L = La; L <= Lb; ++L, base0 += (uint32_t)(S * 96)) {
-        if (!(dbg & 4) && L >= ring_L && L <= ring_end) ring_L = ring_step<W, UNIT>(smd, &cc, &rs, L);
+        // dependencies: predecessor warp done with L-1; ring block landed
+        if (warp > 0 && !(dbg & 16)) wait_geq(&ts.done[warp - 1], L - 1, !(dbg & 64));
+        if (tr) { t1 = clock64(); c_pred += t1 - t0; t0 = t1; }
+        const int need = min(L - T.ilo - klo, T.jhi) / BLK;
+        if (!(dbg & 32)) wait_geq(&ts.landed, need, !(dbg & 64));
+        if (tr) { t1 = clock64(); c_ring += t1 - t0; t0 = t1; }
+        if (!ALIAS && !xcr_valid) {  // alias-free levels: x_ik is this thread's alone
+#pragma unroll
+            for (int s = 0; s < S; ++s) xcr[s] = lds64(sm, G.pik[s]);
+            xcr_valid = true;
+        }
         int pa[S], pc[S], pe[S];
-        const unsigned bits = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
-        const unsigned wbits = __reduce_or_sync(0xffffffffu, bits);
-        // a violated row or a stored dual in this level: replay those slots exactly
-        if (!(dbg & 2) && (wbits != 0u || head < base0 + (uint32_t)(S * 96))) {
+        unsigned bits = 0;
+        if (!(dbg & 8)) bits = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
+        const bool dual_here = head < base0 + (uint32_t)(S * 96);
+        const bool go_cold = __any_sync(0xffffffffu, bits != 0u) || dual_here;
+        if (tr) { t1 = clock64(); c_hot += t1 - t0; t0 = t1; n_cold += go_cold; }
+        if (!(dbg & 2) && go_cold) {
+            // a violated row or a stored dual in this level: replay those slots exactly
+            const unsigned wbits = __reduce_or_sync(0xffffffffu, bits);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const uint32_t bs = base0 + (uint32_t)(s * 96);
@@ -665,7 +689,112 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, double 
                 }
             }
         }
-        if (!(dbg & 1)) __syncthreads();
+        if (tr) { t1 = clock64(); c_cold += t1 - t0; t0 = t1; }
+        __syncwarp();
+        if (lane == 0) {
+            if (go_cold || (dbg & 128)) st_release(&ts.done[warp], L);  // publishes the exact step's writes
+            else st_relaxed(&ts.done[warp], L);
+        }
+        if (tr) { t1 = clock64(); c_rel += t1 - t0; t0 = t1; }
+    }
+    if (tr && lane == 0) {
+        atomicAdd(&cc.trace[TR_PRED_WAIT], c_pred);
+        atomicAdd(&cc.trace[TR_RING_WAIT], c_ring);
+        atomicAdd(&cc.trace[TR_HOT], c_hot);
+        atomicAdd(&cc.trace[TR_COLD], c_cold);
+        atomicAdd(&cc.trace[TR_RELEASE], c_rel);
+        atomicAdd(&cc.trace[TR_LEVELS], (unsigned long long)(Lb - La + 1));
+        atomicAdd(&cc.trace[TR_COLD_CALLS], n_cold);
+    }
+}
+
+// The producer warps (P of them, named barrier 1): keep the j-rings ahead
+// of the fastest compute warp and write back what the slowest has passed.
+// Ring slots of block g are reused by block g + W/BLK, which is loaded only
+// after g was written back.
+__device__ __forceinline__ void producer_bar(int nthreads) {
+    asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+
+template <int W, bool UNIT>
+__device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc, TileSync *ts,
+                                           int nwc, int np, int lo_res, int hi_issued) {
+    const TileDesc &T = cc->T;
+    const int b = cc->b, lane = threadIdx.x & 31;
+    const int ptid = threadIdx.x - nwc * 32, pn = np * 32;
+    double *smd = reinterpret_cast<double *>(sm);
+    double *WR = smd, *WK = smd + b * W;
+    const int xsize = cc->xsize;
+    const int blast = T.jhi / BLK;
+    const int nres = W / BLK;
+#ifndef MP_LOOKAHEAD
+#define MP_LOOKAHEAD 4
+#endif
+    constexpr int LOOKAHEAD = MP_LOOKAHEAD;
+    int landed = hi_issued;  // the prologue landed everything it issued
+    while (true) {
+        // Progress of every compute warp, each read with acquire so their ring
+        // writes up to that level are visible.  Later warps may run ahead of
+        // earlier ones (done[w] <= done[w-1] + 1 bounds them only from above).
+        if (ptid < 32) {
+            int lv = lane < nwc ? ld_acquire(&ts->done[lane]) : 0x3fffffff;
+            int slow = lv, fast = lane < nwc ? lv : -0x3fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                slow = min(slow, __shfl_xor_sync(0xffffffffu, slow, o));
+                fast = max(fast, __shfl_xor_sync(0xffffffffu, fast, o));
+            }
+            if (lane == 0) {
+                ts->pslow = slow + 1;  // next level of the slowest warp
+                ts->pfast = fast + 1;  // next level of the fastest warp
+            }
+        }
+        producer_bar(pn);
+        const int slow = ts->pslow, fast = ts->pfast;
+        if (slow > T.Lend) break;
+        bool busy = false;
+        const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
+        while (lo_res < low_need) {
+            ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, ptid, pn);
+            ++lo_res;
+            busy = true;
+        }
+        const int need_fast = min(fast - T.ilo - T.klo, T.jhi) / BLK;
+        const int want = min(need_fast + LOOKAHEAD, blast);
+        while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
+            ++hi_issued;
+            ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn);
+            if (!UNIT)
+                ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
+                                    WK + xsize, hi_issued, ptid, pn);
+            cp_async_commit();  // one group per block, same sequence in every thread
+            busy = true;
+        }
+        if (landed < hi_issued) {
+            // publish what has landed; only wait for the newest copies when the
+            // fastest warp is about to need them
+            int now;
+            if (need_fast + 1 >= hi_issued - 1) {
+                cp_async_wait_all();
+                now = hi_issued;
+            } else {
+                cp_async_wait_2();
+                now = hi_issued - 2;
+            }
+            if (now > landed) {
+                __threadfence_block();
+                producer_bar(pn);  // every producer thread's copies up to `now` landed
+                if (ptid == 0) st_release(&ts->landed, now);
+                landed = now;
+                busy = true;
+            }
+        }
+        if (!busy) __nanosleep(32);
+        producer_bar(pn);  // ts->pslow/pfast may be rewritten next round
+    }
+    if (ptid == 0) {
+        ts->lo_res = lo_res;
+        ts->hi_issued = hi_issued;
     }
 }
 
@@ -673,10 +802,12 @@ template <int S, int W, bool UNIT>
 __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ CtaConst cc;
-    __shared__ RingState rs;
+    __shared__ TileSync ts;
+    const long long tk0 = clock64();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nt = blockDim.x, nwc = a.nwc, np = nt / 32 - nwc;  // compute / producer warps
     const TileDesc T = a.tiles[blockIdx.x];
-    const int b = a.b, nt = a.nt;
+    const int b = a.b;
     const int bb = b * b;
     const SmemMap<W> M{b};
     // 1024-aligned base (the launch reserves 1 KiB of slack)
@@ -684,7 +815,6 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     double *smd = reinterpret_cast<double *>(sm);
     const int xb = M.xbytes();
     WarpDuals *wds = reinterpret_cast<WarpDuals *>(sm + xb * (UNIT ? 1 : 2));
-    WarpDuals *wd = wds + warp;
     double *WR = smd + M.wr() / 8;
     double *WK = smd + M.wk() / 8;
     double *RK = smd + M.rk() / 8;
@@ -702,34 +832,12 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.nt = nt;
         cc.xsize = xsize;
         cc.dbg = a.dbg;
+        cc.trace = a.trace;
     }
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
+    if (tid < 32) ts.done[tid] = T.Lbeg - 1;
 
-    // --- per-slot geometry --------------------------------------------------
-    // Slot s of this thread owns the pair (i,k) = (ilo + q/b, klo + q%b),
-    // q = tid + s*nt; at level L it processes j = L - (i+k).
-    SlotGeom<S> G;
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        const int q = tid + s * nt;
-        const int ii = q / b, kk = q - (q / b) * b;
-        const int i = T.ilo + ii, k = T.klo + kk;
-        const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
-        const bool ok = q < bb && i <= T.ihi && k <= T.z && js <= je;
-        G.ik8[s] = ok ? 8 * (i + k) : 0;
-        G.off[s] = ok ? i + k + js : 0x3fffffff;
-        G.span[s] = ok ? (unsigned)(je - js) : 0u;
-        G.pik[s] = ok ? M.rk() + 8 * (ii * b + kk) : M.zero();
-        G.wr[s] = ok ? M.wr() + ii * W * 8 : M.zero();
-        G.wk[s] = ok ? M.wk() + kk * W * 8 : M.zero();
-        G.rkr[s] = ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero();
-        G.rkc[s] = ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero();
-    }
-
-    // --- staging prologue ---------------------------------------------------
-    // Level L reads j in [L - ihi - z, L - ilo - klo] (clipped to J); keep
-    // those j-blocks landed, one more block in flight, and write blocks back
-    // once the wavefront bottom has passed them.
+    // --- staging prologue (all threads) -----------------------------------
     rk_block<true>(T, b, a.ld, a.x, RK, tid, nt);
     if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt);
     const int blast = T.jhi / BLK;
@@ -742,53 +850,75 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
                                 bk, tid, nt);
     }
     cp_async_commit();
-    if (tid == 0) {
-        rs.lo_res = lo0;
-        rs.hi_issued = hi0;
-        rs.hi_landed = hi0;
-        rs.blast = blast;
-    }
-    // --- dual streams --------------------------------------------------------
-    rd_init(wd, a.rp, T.stream0 + warp, lane);
+    if (tid == 0) ts.landed = hi0;
+    WarpDuals *wd = wds + (warp < nwc ? warp : 0);
+    if (warp < nwc) rd_init(wd, a.rp, T.stream0 + warp, lane);
     cp_async_wait_all();
     __syncthreads();
+    const long long tk1 = clock64();
 
     double viol = 0.0;
-    const int ihi = T.ihi, klo = T.klo;
-    // the top j = L - ilo - klo leaves the landed blocks at ring_L
-    int ring_L = BLK * (hi0 + 1) + T.ilo + T.klo;
-    const int ring_end = T.jhi + T.ilo + T.klo;  // top j past jhi: nothing more to land
-    uint32_t head = wd->head;
-    // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or K)
-    // iff L in (2*ihi + z, 2*klo + ilo).
-    const int mid_a = max(2 * ihi + T.z + 1, T.Lbeg);
-    const int mid_b = min(2 * klo + T.ilo - 1, T.Lend);
-    if (mid_a <= mid_b) {
-        sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
-                                ring_L, head, viol);
-        sweep<S, W, UNIT, false>(mid_a, mid_b, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
-                                 ring_L, head, viol);
-        sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
-                                ring_L, head, viol);
+    if (warp >= nwc) {
+        ring_producer<W, UNIT>(sm, &cc, &ts, nwc, np, lo0, hi0);
     } else {
-        sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, smd, G, cc, rs, wd, b, ihi, klo, ring_end,
-                                ring_L, head, viol);
+        // --- per-slot geometry: q = warp*32*S + s*32 + lane -> (i,k) -------
+        SlotGeom<S> G;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int q = warp * 32 * S + s * 32 + lane;
+            const int ii = q / b, kk = q - (q / b) * b;
+            const int i = T.ilo + ii, k = T.klo + kk;
+            const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
+            const bool ok = q < bb && i <= T.ihi && k <= T.z && js <= je;
+            G.ik8[s] = ok ? 8 * (i + k) : 0;
+            G.off[s] = ok ? i + k + js : 0x3fffffff;
+            G.span[s] = ok ? (unsigned)(je - js) : 0u;
+            G.pik[s] = ok ? M.rk() + 8 * (ii * b + kk) : M.zero();
+            G.wr[s] = ok ? M.wr() + ii * W * 8 : M.zero();
+            G.wk[s] = ok ? M.wk() + kk * W * 8 : M.zero();
+            G.rkr[s] = ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero();
+            G.rkc[s] = ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero();
+        }
+        const int ihi = T.ihi, klo = T.klo;
+        uint32_t head = wd->head;
+        // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or
+        // K) iff L in (2*ihi + z, 2*klo + ilo).
+        const int mid_a = max(2 * ihi + T.z + 1, T.Lbeg);
+        const int mid_b = min(2 * klo + T.ilo - 1, T.Lend);
+        if (mid_a <= mid_b) {
+            sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
+            sweep<S, W, UNIT, false>(mid_a, mid_b, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
+            sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
+        } else {
+            sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
+        }
     }
 
-    // --- epilogue: write back everything still staged ------------------------
-    cp_async_wait_all();
+    // --- epilogue: write back everything still staged ----------------------
     __syncthreads();
-    for (int bk = rs.lo_res; bk <= rs.hi_issued; ++bk)
+    const long long tk2 = clock64();
+    for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk)
         ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
     rk_block<false>(T, b, a.ld, a.x, RK, tid, nt);
-    wr_finish(wd, a.wp, a.ctr, T.stream0 + warp, lane);
-    viol = warp_max(viol);
-    if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
+    if (a.trace) {
+        __syncthreads();
+        if (tid == 0) {
+            atomicAdd(&a.trace[TR_PROLOGUE], (unsigned long long)(tk1 - tk0));
+            atomicAdd(&a.trace[TR_LOOP], (unsigned long long)(tk2 - tk1));
+            atomicAdd(&a.trace[TR_EPILOGUE], (unsigned long long)(clock64() - tk2));
+            atomicAdd(&a.trace[TR_CTAS], 1ull);
+        }
+    }
+    if (warp < nwc) {
+        wr_finish(wd, a.wp, a.ctr, T.stream0 + warp, lane);
+        viol = warp_max(viol);
+        if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
+    }
 }
 
 // dynamic shared memory of one CTA (+1 KiB alignment slack)
 inline size_t tile_smem_bytes(int b, int W, bool unit, int nt) {
-    const size_t xb = W == 64 ? SmemMap<64>{b}.xbytes() : SmemMap<128>{b}.xbytes();
+    const size_t xb = W == 256 ? SmemMap<256>{b}.xbytes() : SmemMap<128>{b}.xbytes();
     return 1024 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
 }
 

@@ -93,7 +93,7 @@ struct mp_handle {
     double *snap_x = nullptr, *snap_f = nullptr, *snap_pu = nullptr, *snap_pl = nullptr;
 
     // schedule
-    int S = 1, NT = 32, W = 64;
+    int S = 1, NT = 64, NWC = 1, NPW = 1, W = 128;
     size_t smem = 0;
     std::vector<TileDesc> tiles;
     std::vector<int64_t> round_off, round_cnt;
@@ -119,6 +119,7 @@ struct mp_handle {
     double metric_ms = 0.0, pair_ms = 0.0;
     int64_t launches = 0;
     unsigned long long *d_scan = nullptr;
+    unsigned long long *trace = nullptr;  // mp_trace buffer (TR_NSLOTS counters)
     void *flush = nullptr;
     size_t flush_bytes = 0;
 
@@ -136,6 +137,7 @@ struct mp_handle {
         cudaFree(ctr);
         cudaFree(d_stats);
         cudaFree(d_scan);
+        cudaFree(trace);
         cudaFree(flush);
         if (h_stats) cudaFreeHost(h_stats);
         for (auto &e : ev)
@@ -171,9 +173,7 @@ int launch_tiles_t(mp_handle *h, const TileArgs &a, int ntiles) {
 
 template <int S>
 int launch_tiles_s(mp_handle *h, const TileArgs &a, int ntiles) {
-    if (h->W == 64)
-        return h->unit_x ? launch_tiles_t<S, 64, true>(h, a, ntiles)
-                         : launch_tiles_t<S, 64, false>(h, a, ntiles);
+    if (h->W == 256) return launch_tiles_t<S, 256, true>(h, a, ntiles);
     return h->unit_x ? launch_tiles_t<S, 128, true>(h, a, ntiles)
                      : launch_tiles_t<S, 128, false>(h, a, ntiles);
 }
@@ -218,6 +218,8 @@ int enqueue_pass(mp_handle *h) {
     ta.ld = h->ld;
     ta.b = h->b;
     ta.nt = h->NT;
+    ta.nwc = h->NWC;
+    ta.trace = h->trace;
     ta.eps = h->eps;
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[wp];
@@ -282,7 +284,7 @@ Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
     const uint32_t lvl = key / per_level, rem = key % per_level;
     const int s = (int)(rem / 96u), r2 = (int)(rem % 96u);
     const int lane = r2 / 3, kind = r2 % 3;
-    const int64_t q = (int64_t)w * 32 + lane + (int64_t)s * h->NT;
+    const int64_t q = (int64_t)w * 32 * h->S + (int64_t)s * 32 + lane;
     const int64_t ii = q / h->b, kk = q % h->b;
     Decoded d;
     d.i = T.ilo + ii;
@@ -366,15 +368,22 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
 
     // ---- schedule (schedule.tiled_rounds, schedule.py:117-153) -------------
     {
-        // threads per CTA: env MP_CTA_THREADS (tuning), default 512
-        int target = MAX_CTA_THREADS;
-        if (const char *e = getenv("MP_CTA_THREADS")) target = std::max(32, std::min(MAX_CTA_THREADS, atoi(e)));
-        h->S = std::min((b * b + target - 1) / target, MAX_SLOTS);
-        h->NT = ((b * b + h->S - 1) / h->S + 31) / 32 * 32;
-        if (h->NT > MAX_CTA_THREADS) return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d needs too many threads", b));
+        // S slots per thread, NWC compute warps + 1 producer warp per CTA.
+        // b <= 32*S keeps every lattice neighbour in the same or previous warp.
+        int S = std::max(1, (b + 31) / 32);
+        while ((b * b + 32 * S - 1) / (32 * S) > MAX_CTA_THREADS / 32 - 1) ++S;
+        if (const char *e = getenv("MP_SLOTS")) S = std::max(S, atoi(e));
+        if (S > MAX_SLOTS) return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d needs too many slots", b));
+        h->S = S;
+        h->NWC = (b * b + 32 * S - 1) / (32 * S);
+        h->NPW = std::min(3, MAX_CTA_THREADS / 32 - h->NWC);  // producer warps
+        if (const char *e = getenv("MP_PRODUCERS")) h->NPW = std::max(1, std::min(h->NPW, atoi(e)));
+        h->NT = 32 * (h->NWC + h->NPW);
     }
-    h->W = b <= 16 ? 64 : 128;
-    const int nwarps = h->NT / 32;
+    // ring width: 256 j-slots (16 blocks) when it fits, else 128
+    h->W = (h->unit_x && tile_smem_bytes(b, 256, true, h->NT) <= 225 * 1024) ? 256 : 128;
+    if (const char *e = getenv("MP_RING_W")) h->W = (atoi(e) == 256 && h->W == 256) ? 256 : 128;
+    const int nwarps = h->NWC;  // one dual stream per compute warp
     h->nib = (n + b - 1) / b + 2;
     h->nkb = (n - 1) / b + 2;
     h->tile_of_blk.assign((size_t)(h->nib * h->nkb), -1);
@@ -594,7 +603,7 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
     if (h->nstreams)
         CK(cudaMemcpyAsync(hh.data(), P.head, hh.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    const int nwarps = h->NT / 32;
+    const int nwarps = h->NWC;
     const int64_t n = h->n;
     int64_t outpos = 0;
     struct E {
@@ -665,8 +674,7 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         if (t < 0) return fail(MP_ERR_ARG, "key outside schedule");
         const TileDesc &T = h->tiles[(size_t)t];
         const int64_t q = (i - T.ilo) * b + (k - T.klo);
-        const int64_t s = q / h->NT, tt = q % h->NT;
-        const int64_t w = tt / 32, lane = tt % 32;
+        const int64_t w = q / (32 * h->S), s = (q % (32 * h->S)) / 32, lane = q % 32;
         const int64_t lvl = i + j + k - T.Lbeg;
         const uint32_t key32 = (uint32_t)(((lvl * h->S + s) * 96) + lane * 3 + kind);
         ents.push_back({T.stream0 + w, {key32, vals[e]}});
@@ -755,6 +763,29 @@ int mp_get_timing(mp_handle *h, double *metric_ms, double *pair_ms, int64_t *lau
     if (metric_ms) *metric_ms = h->metric_ms;
     if (pair_ms) *pair_ms = h->pair_ms;
     if (launches) *launches = h->launches;
+    return MP_OK;
+}
+
+int mp_trace(mp_handle *h, int32_t enable, uint64_t *out, int32_t nslots) {
+    g_err.clear();
+    if (!h) return fail(MP_ERR_ARG, "null handle");
+    CK(cudaSetDevice(h->dev));
+    if (enable && !h->trace) {
+        CK(cudaMalloc(&h->trace, TR_NSLOTS * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(h->trace, 0, TR_NSLOTS * sizeof(unsigned long long), h->st));
+    }
+    if (out && h->trace) {
+        unsigned long long buf[TR_NSLOTS];
+        CK(cudaMemcpyAsync(buf, h->trace, sizeof(buf), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        for (int i = 0; i < nslots && i < TR_NSLOTS; ++i) out[i] = buf[i];
+        CK(cudaMemsetAsync(h->trace, 0, sizeof(buf), h->st));
+    }
+    if (!enable && h->trace) {
+        CK(cudaStreamSynchronize(h->st));
+        cudaFree(h->trace);
+        h->trace = nullptr;
+    }
     return MP_OK;
 }
 
