@@ -218,18 +218,15 @@ def verify_independence(rounds, n):
 # device mapping (mirrors mp_create in csrc/mp_solver.cu)
 # ---------------------------------------------------------------------------
 
-def _max_threads(slots):
-    return 1024 if slots == 1 else (832 if slots == 2 else 768)
-
-
-def cta_shape(b):
-    """(slots per thread S, threads per CTA) for tile size b."""
-    s = 1
-    while True:
-        nt = ((b * b + s - 1) // s + 31) // 32 * 32
-        if nt <= _max_threads(s):
-            return s, nt
+def cta_shape(b, max_threads=512):
+    """(slots per thread S, compute warps, producer warps) of mp_create: b*b
+    (i,k) pairs map to q = warp*32*S + s*32 + lane, b <= 32*S so lattice
+    neighbours sit in the same or the previous warp."""
+    s = max(1, (b + 31) // 32)
+    while (b * b + 32 * s - 1) // (32 * s) > max_threads // 32 - 1:
         s += 1
+    nwc = (b * b + 32 * s - 1) // (32 * s)
+    return s, nwc, min(3, max_threads // 32 - nwc)
 
 
 def launch_plan(n, b):

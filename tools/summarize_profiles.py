@@ -1,0 +1,117 @@
+"""Summarise a round's ncu outputs (gpurun_out/) into profiles/<tag>_*.
+
+  python tools/summarize_profiles.py r01
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+
+def read_ncu_csv(path):
+    txt = open(path).read()
+    start = txt.find('"ID"')
+    rows = list(csv.reader(io.StringIO(txt[start:])))
+    hdr = rows[0]
+    return [dict(zip(hdr, r)) for r in rows[1:] if len(r) == len(hdr)]
+
+
+def num(x):
+    try:
+        return float(x.replace(",", ""))
+    except ValueError:
+        return 0.0
+
+
+def launches(tag):
+    rows = read_ncu_csv(os.path.join(OUT, f"launches_{tag}.csv"))
+    per = defaultdict(lambda: [0, 0.0])
+    for r in rows:
+        if r["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        k = r["Kernel Name"].split("(")[0]
+        unit = r["Metric Unit"]
+        v = num(r["Metric Value"]) * (1e-3 if unit == "ns" else (1.0 if unit == "us" else 1e3))
+        per[k][0] += 1
+        per[k][1] += v
+    tot = sum(v[1] for v in per.values())
+    lines = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for k, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"| `{k}` | {c} | {t:.1f} | {t / tot * 100:.2f}% |")
+    return "\n".join(lines), per, tot
+
+
+def tile_dram(tag):
+    rows = read_ncu_csv(os.path.join(OUT, f"tile_dram_{tag}.csv"))
+    per = defaultdict(dict)
+    for r in rows:
+        per[r["ID"]][r["Metric Name"]] = (num(r["Metric Value"]), r["Metric Unit"])
+    def b(v):
+        val, unit = v
+        return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    n = len(per)
+    rd = sum(b(d["dram__bytes_read.sum"]) for d in per.values())
+    wr = sum(b(d["dram__bytes_write.sum"]) for d in per.values())
+    lts = sum(b(d["lts__t_bytes.sum"]) for d in per.values())
+    dur = sum(d["gpu__time_duration.sum"][0] * (1e-3 if d["gpu__time_duration.sum"][1] == "ns" else 1)
+              for d in per.values())
+    inst = sum(d["smsp__inst_executed.sum"][0] for d in per.values())
+    return {"launches": n, "dram_read_bytes": rd, "dram_write_bytes": wr,
+            "dram_bytes_per_launch": (rd + wr) / max(n, 1), "l2_bytes_per_launch": lts / max(n, 1),
+            "duration_us_total": dur, "warp_instructions_total": inst}
+
+
+def full_summary(tag):
+    rep = os.path.join(OUT, f"prof_tile_{tag}.ncu-rep")
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr = rows[0]
+    keep = ["Duration", "Elapsed Cycles", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate",
+            "L2 Hit Rate", "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
+            "Dynamic Shared Memory Per Block", "Block Size", "Grid Size", "Achieved Active Warps Per SM",
+            "Warp Cycles Per Issued Instruction", "Executed Instructions", "No Eligible"]
+    out = {}
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") in keep:
+            out[d["Metric Name"]] = f'{d["Metric Value"]} {d["Metric Unit"]}'.strip()
+    return out
+
+
+def main(tag):
+    os.makedirs(PROF, exist_ok=True)
+    table, per, tot = launches(tag)
+    dram = tile_dram(tag)
+    full = full_summary(tag)
+    stall = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
+                            os.path.join(OUT, f"prof_tile_{tag}.ncu-rep"), "25"],
+                           capture_output=True, text=True).stdout
+    with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
+        fh.write(f"# ncu summary, round {tag}\n\n")
+        fh.write("## Launch list of `python bench.py --steps 3 --warmup 3 --no-cpu` "
+                 "(`--metrics gpu__time_duration.sum --clock-control none`; cold-cache, serialised)\n\n")
+        fh.write(table + "\n\n")
+        fh.write("## tile_round_kernel, all 50 launches of pass 4 (config 2, n=1000, b=40)\n\n")
+        fh.write("```\n" + json.dumps(dram, indent=2) + "\n```\n\n")
+        fh.write("## Full capture (`--set full`), biggest round of pass 3\n\n```\n")
+        for k, v in full.items():
+            fh.write(f"{k:40s} {v}\n")
+        fh.write("```\n\n## Per-source-line instruction share and stall samples\n\n```\n" + stall + "```\n")
+    data = {"config2_b40": {"dram_bytes_per_launch": dram["dram_bytes_per_launch"],
+                            "l2_bytes_per_launch": dram["l2_bytes_per_launch"],
+                            "launches_measured": dram["launches"], "source": f"{tag}_ncu_summary.md"}}
+    with open(os.path.join(PROF, "ncu_tile_kernel.json"), "w") as fh:
+        json.dump(data, fh, indent=2)
+    print(open(os.path.join(PROF, f"{tag}_ncu_summary.md")).read()[:3000])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
