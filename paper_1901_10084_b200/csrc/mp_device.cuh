@@ -114,7 +114,8 @@ struct TileArgs {
 // trace slots (cycles summed over warps / CTAs; see tools/trace_pass.py)
 enum TraceSlot {
     TR_PRED_WAIT = 0, TR_RING_WAIT, TR_HOT, TR_COLD, TR_RELEASE, TR_LEVELS, TR_COLD_CALLS,
-    TR_PROLOGUE = 8, TR_LOOP, TR_EPILOGUE, TR_PROD_BUSY, TR_CTAS, TR_NSLOTS = 16
+    TR_PROLOGUE = 8, TR_LOOP, TR_EPILOGUE, TR_EPI_BLOCKS, TR_CTAS, TR_C_LOOKUP, TR_C_MATH,
+    TR_C_APPEND, TR_NSLOTS = 16
 };
 
 // Per-warp dual-stream state, in shared memory.
@@ -195,6 +196,17 @@ __device__ __forceinline__ double warp_max(double v) {
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
+// 32-bit shared-window addresses: the per-slot constants already hold the
+// absolute address, so the hot loop issues LDS [R] with no base add
+__device__ __forceinline__ double ld_sh(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void st_sh(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
@@ -459,19 +471,22 @@ __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, d
 // ---------------------------------------------------------------------------
 // cold path: a warp replays one slot of one level with the full step
 // ---------------------------------------------------------------------------
-// pa/pc/pe are the byte offsets of x_ij, x_ik, x_jk the hot path computed
+// pa/pc/pe are the shared addresses of x_ij, x_ik, x_jk the hot path computed
 // (the zero row for inactive slots, where every row value is 0 and no dual
 // exists, so the exact step is a no-op there).
 template <int W, bool UNIT>
 __device__ __noinline__ double cold_slot(unsigned char *sm, const CtaConst *cc, WarpDuals *wd,
                                          uint32_t base, int pa, int pc, int pe, double viol) {
     const int tid = threadIdx.x, lane = tid & 31;
+#ifdef MP_TRACE
+    long long q0 = clock64();
+#endif
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     if (wd->head < base + 96u) rd_lookup(wd, cc->rp, base, lane, y0, y1, y2);
-    double *xa = reinterpret_cast<double *>(sm + pa);
-    double *xc = reinterpret_cast<double *>(sm + pc);
-    double *xe = reinterpret_cast<double *>(sm + pe);
-    double p = *xa, c = *xc, e = *xe;
+#ifdef MP_TRACE
+    long long q1 = clock64();
+#endif
+    double p = ld_sh(pa), c = ld_sh(pc), e = ld_sh(pe);
     const double d0 = __dsub_rn(__dsub_rn(p, c), e);
     const double d1 = __dsub_rn(__dsub_rn(c, p), e);
     const double d2 = __dsub_rn(__dsub_rn(e, p), c);
@@ -480,19 +495,30 @@ __device__ __noinline__ double cold_slot(unsigned char *sm, const CtaConst *cc, 
         double wa = 1.0, wc = 1.0, we = 1.0;
         if (!UNIT) {
             const int xb = cc->xsize * 8;  // winv staging mirrors the x layout
-            wa = *reinterpret_cast<const double *>(sm + xb + pa);
-            wc = *reinterpret_cast<const double *>(sm + xb + pc);
-            we = *reinterpret_cast<const double *>(sm + xb + pe);
+            wa = ld_sh(pa + xb);
+            wc = ld_sh(pc + xb);
+            we = ld_sh(pe + xb);
         }
         const double eps = cc->eps;
         t0 = dykstra_row<UNIT>(p, c, e, wa, wc, we, y0, eps, viol);  // IJ: x_ij <= x_ik + x_jk
         t1 = dykstra_row<UNIT>(c, p, e, wc, wa, we, y1, eps, viol);  // IK: x_ik <= x_ij + x_jk
         t2 = dykstra_row<UNIT>(e, p, c, we, wa, wc, y2, eps, viol);  // JK: x_jk <= x_ij + x_ik
-        *xa = p;
-        *xc = c;
-        *xe = e;
+        st_sh(pa, p);
+        st_sh(pc, c);
+        st_sh(pe, e);
     }
+#ifdef MP_TRACE
+    long long q2 = clock64();
+#endif
     wr_append(wd, cc->wp, cc->ctr, cc->T.stream0 + (tid >> 5), base, lane, t0, t1, t2);
+#ifdef MP_TRACE
+    if (cc->trace && lane == 0) {
+        long long q3 = clock64();
+        atomicAdd(&cc->trace[TR_C_LOOKUP], (unsigned long long)(q1 - q0));
+        atomicAdd(&cc->trace[TR_C_MATH], (unsigned long long)(q2 - q1));
+        atomicAdd(&cc->trace[TR_C_APPEND], (unsigned long long)(q3 - q2));
+    }
+#endif
     return viol;
 }
 
@@ -527,6 +553,7 @@ struct SlotGeom {
     int wk[S];        // byte offset of WK row kk (or zero row)
     int rkr[S];       // RK byte offset of x_ij when j in K:  rkr + 8j
     int rkc[S];       // RK byte offset of x_jk when j in R:  8*b*j + rkc
+    int zero;         // shared address of the zero row
 };
 
 __device__ __forceinline__ double lds64(const unsigned char *base, int off) {
@@ -555,13 +582,15 @@ __device__ __forceinline__ unsigned triplet_violated(double a, double c, double 
     return r;
 }
 
-// Hot part of one level: bit s set when slot s saw a violated row; the
-// slots' byte offsets are left in pa/pc/pe for the cold path.
-// Branch-free: inactive slots read the zero row (all row values 0).
+// Hot part of one level: true when some slot of this thread has a violated
+// row; the slots' byte offsets are left in pa/pc/pe for the cold path.
+// Branch-free: inactive slots read the zero row (all row values 0).  With
+// t = fl(a - c), u = fl(e - a):  (d0 > 0 || d1 > 0) <=> |t| > e  and
+// d2 > 0 <=> u > c, exactly (see triplet_violated).
 template <int S, int W, bool ALIAS>
-__device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const SlotGeom<S> &G, int L,
-                                              int b, int ihi, int klo, int (&pa)[S], int (&pc)[S],
-                                              int (&pe)[S], const double (&xcr)[S]) {
+__device__ __forceinline__ bool level_hot(const unsigned char *sm, const SlotGeom<S> &G, int L,
+                                          int b, int ihi, int klo, int (&pa)[S], int (&pc)[S],
+                                          int (&pe)[S], const double (&xcr)[S]) {
     const int L8 = L * 8;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -572,10 +601,9 @@ __device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const Slo
             const int j = j8 >> 3;
             int a0 = j >= klo ? G.rkr[s] + j8 : (jm | G.wr[s]);
             int e0 = j <= ihi ? j * (8 * b) + G.rkc[s] : (jm | G.wk[s]);
-            const int z = SmemMap<W>{b}.zero();
-            pa[s] = act ? a0 : z;
-            pe[s] = act ? e0 : z;
-            pc[s] = act ? G.pik[s] : z;
+            pa[s] = act ? a0 : G.zero;
+            pe[s] = act ? e0 : G.zero;
+            pc[s] = act ? G.pik[s] : G.zero;
         } else {
             pa[s] = jm | G.wr[s];
             pe[s] = jm | G.wk[s];
@@ -585,15 +613,19 @@ __device__ __forceinline__ unsigned level_hot(const unsigned char *sm, const Slo
     double xa[S], xc[S], xe[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        xa[s] = lds64(sm, pa[s]);
+        xa[s] = ld_sh(pa[s]);
         // alias-free levels: x_ik belongs to this thread alone, kept in a register
-        xc[s] = ALIAS ? lds64(sm, pc[s]) : xcr[s];
-        xe[s] = lds64(sm, pe[s]);
+        xc[s] = ALIAS ? ld_sh(pc[s]) : xcr[s];
+        xe[s] = ld_sh(pe[s]);
     }
-    unsigned bits = 0;
+    bool bad = false;
 #pragma unroll
-    for (int s = 0; s < S; ++s) bits |= triplet_violated(xa[s], xc[s], xe[s]) << s;
-    return bits;
+    for (int s = 0; s < S; ++s) {
+        const double t = __dsub_rn(xa[s], xc[s]);
+        const double u = __dsub_rn(xe[s], xa[s]);
+        bad = bad | (fabs(t) > xe[s]) | (u > xc[s]);
+    }
+    return bad;
 }
 
 // ---------------------------------------------------------------------------
@@ -640,17 +672,72 @@ struct TileSync {
     int pslow, pfast;  // producer-internal broadcast
 };
 
+// Re-derive on the cold path whether slot s has a violated row.
+__device__ __forceinline__ bool slot_violated(const unsigned char *sm, int pa, int pc, int pe) {
+    const double a = ld_sh(pa), c = ld_sh(pc), e = ld_sh(pe);
+    return (fabs(__dsub_rn(a, c)) > e) | (__dsub_rn(e, a) > c);
+}
+
+// spin until *p >= v (acquire); returns the value seen
+__device__ __forceinline__ int wait_geq_v(const int *p, int v) {
+    int x = ld_acquire(p);
+    while (x < v) {
+        __nanosleep(20);
+        x = ld_acquire(p);
+    }
+    return x;
+}
+
+#ifndef MP_BATCH
+#define MP_BATCH 4
+#endif
+
+// One level done exactly the old way: hot check, then the exact step for the
+// slots that need it.  Returns whether the cold path ran.
+template <int S, int W, bool UNIT, bool ALIAS>
+__device__ __forceinline__ bool level_full(int L, uint32_t base0, unsigned char *sm,
+                                           const SlotGeom<S> &G, CtaConst &cc, WarpDuals *wd,
+                                           int b, int ihi, int klo, double (&xcr)[S],
+                                           uint32_t &head, double &viol) {
+    int pa[S], pc[S], pe[S];
+    const bool bad = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
+    const bool go_cold = __any_sync(0xffffffffu, bad) || head < base0 + (uint32_t)(S * 96);
+    if (go_cold) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t bs = base0 + (uint32_t)(s * 96);
+            if (__any_sync(0xffffffffu, bad && slot_violated(sm, pa[s], pc[s], pe[s])) ||
+                head < bs + 96u) {
+                viol = cold_slot<W, UNIT>(sm, &cc, wd, bs, pa[s], pc[s], pe[s], viol);
+                head = wd->head;
+                if (!ALIAS) xcr[s] = ld_sh(pc[s]);  // the exact step may move x_ik
+            }
+        }
+    }
+    return go_cold;
+}
+
+// Sweep levels [La, Lb] of one phase.  Levels are taken in batches of U: in
+// the common case nothing moves, so the U levels' checks read only data
+// that is final (the predecessor warp is done with the batch's last level
+// minus one) and can be issued together; progress is published once per
+// batch.  If some level of the batch needs the exact step, the batch is
+// finished level by level from that level on (later levels re-checked after
+// the update).
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const SlotGeom<S> &G,
                                       CtaConst &cc, TileSync &ts, WarpDuals *wd, int warp, int b,
                                       int ihi, int klo, uint32_t &head, double &viol) {
     if (La > Lb) return;
+    constexpr int U = MP_BATCH;
+    constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
     const TileDesc &T = cc.T;
     const int lane = threadIdx.x & 31;
-    uint32_t base0 = (uint32_t)(La - T.Lbeg) * (uint32_t)(S * 96);
     double xcr[S];
-    bool xcr_valid = false;
-    const int dbg = cc.dbg;  // TEMP experiment switches
+    if (!ALIAS) {  // alias-free levels: x_ik is this thread's alone
+#pragma unroll
+        for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
+    }
 #ifdef MP_TRACE
     const bool tr = cc.trace != nullptr;
 #else
@@ -658,43 +745,52 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #endif
     unsigned long long c_pred = 0, c_ring = 0, c_hot = 0, c_cold = 0, c_rel = 0, n_cold = 0;
     long long t0 = tr ? clock64() : 0, t1;
-    for (int L = La; L <= Lb; ++L, base0 += (uint32_t)(S * 96)) {
-        // dependencies: predecessor warp done with L-1; ring block landed
-        if (warp > 0 && !(dbg & 16)) wait_geq(&ts.done[warp - 1], L - 1, !(dbg & 64));
+    const int *pred_flag = &ts.done[warp > 0 ? warp - 1 : 0];
+    int pred_seen = warp > 0 ? ld_acquire(pred_flag) : 0x3fffffff;
+    int landed_seen = ld_acquire(&ts.landed);
+    const int jtop0 = T.ilo + klo;  // top j at level L is L - jtop0
+    for (int L = La; L <= Lb; L += U) {
+        const int Le = min(L + U - 1, Lb);
+        const uint32_t base0 = (uint32_t)(L - T.Lbeg) * PER_LEVEL;
+        // dependencies of the whole batch: predecessor done with Le-1; ring landed
+#ifndef MP_EXP_NOWAIT
+        if (pred_seen < Le - 1) pred_seen = wait_geq_v(pred_flag, Le - 1);
+#endif
         if (tr) { t1 = clock64(); c_pred += t1 - t0; t0 = t1; }
-        const int need = min(L - T.ilo - klo, T.jhi) / BLK;
-        if (!(dbg & 32)) wait_geq(&ts.landed, need, !(dbg & 64));
+        const int need = min(Le - jtop0, T.jhi) >> 4;
+#ifndef MP_EXP_NOWAIT
+        if (landed_seen < need) landed_seen = wait_geq_v(&ts.landed, need);
+#endif
         if (tr) { t1 = clock64(); c_ring += t1 - t0; t0 = t1; }
-        if (!ALIAS && !xcr_valid) {  // alias-free levels: x_ik is this thread's alone
+        const int pf = warp > 0 ? ld_acquire(pred_flag) : 0x3fffffff;  // for the next batch
+        bool bad = false;
 #pragma unroll
-            for (int s = 0; s < S; ++s) xcr[s] = lds64(sm, G.pik[s]);
-            xcr_valid = true;
-        }
-        int pa[S], pc[S], pe[S];
-        unsigned bits = 0;
-        if (!(dbg & 8)) bits = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
-        const bool dual_here = head < base0 + (uint32_t)(S * 96);
-        const bool go_cold = __any_sync(0xffffffffu, bits != 0u) || dual_here;
-        if (tr) { t1 = clock64(); c_hot += t1 - t0; t0 = t1; n_cold += go_cold; }
-        if (!(dbg & 2) && go_cold) {
-            // a violated row or a stored dual in this level: replay those slots exactly
-            const unsigned wbits = __reduce_or_sync(0xffffffffu, bits);
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const uint32_t bs = base0 + (uint32_t)(s * 96);
-                if (((wbits >> s) & 1u) || head < bs + 96u) {
-                    viol = cold_slot<W, UNIT>(sm, &cc, wd, bs, pa[s], pc[s], pe[s], viol);
-                    head = wd->head;
-                    if (!ALIAS) xcr[s] = lds64(sm, pc[s]);  // the exact step may move x_ik
-                }
+        for (int u = 0; u < U; ++u) {
+            if (L + u <= Le) {
+                int pa[S], pc[S], pe[S];
+                bad |= level_hot<S, W, ALIAS>(sm, G, L + u, b, ihi, klo, pa, pc, pe, xcr);
             }
+        }
+        const bool wbad = __any_sync(0xffffffffu, bad);
+        const uint32_t lim = base0 + (uint32_t)(Le - L + 1) * PER_LEVEL;
+        const bool go_cold = wbad || head < lim;
+        if (tr) { t1 = clock64(); c_hot += t1 - t0; t0 = t1; n_cold += go_cold; }
+        if (go_cold) {
+            // first level of the batch that may need the exact step (level_full
+            // re-checks each level, so starting early is only slower)
+            int first = wbad ? L : Le + 1;
+            if (head < lim) first = min(first, L + (int)((head - base0) / PER_LEVEL));
+            for (int Lc = first; Lc <= Le; ++Lc)
+                level_full<S, W, UNIT, ALIAS>(Lc, (uint32_t)(Lc - T.Lbeg) * PER_LEVEL, sm, G, cc,
+                                              wd, b, ihi, klo, xcr, head, viol);
         }
         if (tr) { t1 = clock64(); c_cold += t1 - t0; t0 = t1; }
         __syncwarp();
         if (lane == 0) {
-            if (go_cold || (dbg & 128)) st_release(&ts.done[warp], L);  // publishes the exact step's writes
-            else st_relaxed(&ts.done[warp], L);
+            if (go_cold) st_release(&ts.done[warp], Le);  // publishes the exact steps' writes
+            else st_relaxed(&ts.done[warp], Le);
         }
+        pred_seen = max(pred_seen, pf);
         if (tr) { t1 = clock64(); c_rel += t1 - t0; t0 = t1; }
     }
     if (tr && lane == 0) {
@@ -810,8 +906,10 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const int b = a.b;
     const int bb = b * b;
     const SmemMap<W> M{b};
-    // 1024-aligned base (the launch reserves 1 KiB of slack)
-    unsigned char *sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    // base aligned to W*8 bytes (the launch reserves the slack) so ring rows
+    // are W*8-aligned shared addresses and a slot address is one LOP3
+    unsigned char *sm = smem_raw + ((W * 8 - (smem_u32(smem_raw) & (W * 8 - 1))) & (W * 8 - 1));
+    const int B32 = (int)smem_u32(sm);
     double *smd = reinterpret_cast<double *>(sm);
     const int xb = M.xbytes();
     WarpDuals *wds = reinterpret_cast<WarpDuals *>(sm + xb * (UNIT ? 1 : 2));
@@ -873,12 +971,13 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
             G.ik8[s] = ok ? 8 * (i + k) : 0;
             G.off[s] = ok ? i + k + js : 0x3fffffff;
             G.span[s] = ok ? (unsigned)(je - js) : 0u;
-            G.pik[s] = ok ? M.rk() + 8 * (ii * b + kk) : M.zero();
-            G.wr[s] = ok ? M.wr() + ii * W * 8 : M.zero();
-            G.wk[s] = ok ? M.wk() + kk * W * 8 : M.zero();
-            G.rkr[s] = ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero();
-            G.rkc[s] = ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero();
+            G.pik[s] = B32 + (ok ? M.rk() + 8 * (ii * b + kk) : M.zero());
+            G.wr[s] = B32 + (ok ? M.wr() + ii * W * 8 : M.zero());
+            G.wk[s] = B32 + (ok ? M.wk() + kk * W * 8 : M.zero());
+            G.rkr[s] = B32 + (ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero());
+            G.rkc[s] = B32 + (ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero());
         }
+        G.zero = B32 + M.zero();
         const int ihi = T.ihi, klo = T.klo;
         uint32_t head = wd->head;
         // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or
@@ -900,15 +999,18 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk)
         ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
     rk_block<false>(T, b, a.ld, a.x, RK, tid, nt);
+#ifdef MP_TRACE
     if (a.trace) {
         __syncthreads();
         if (tid == 0) {
             atomicAdd(&a.trace[TR_PROLOGUE], (unsigned long long)(tk1 - tk0));
             atomicAdd(&a.trace[TR_LOOP], (unsigned long long)(tk2 - tk1));
             atomicAdd(&a.trace[TR_EPILOGUE], (unsigned long long)(clock64() - tk2));
+            atomicAdd(&a.trace[TR_EPI_BLOCKS], (unsigned long long)(ts.hi_issued - ts.lo_res + 1));
             atomicAdd(&a.trace[TR_CTAS], 1ull);
         }
     }
+#endif
     if (warp < nwc) {
         wr_finish(wd, a.wp, a.ctr, T.stream0 + warp, lane);
         viol = warp_max(viol);
@@ -916,10 +1018,10 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     }
 }
 
-// dynamic shared memory of one CTA (+1 KiB alignment slack)
+// dynamic shared memory of one CTA
 inline size_t tile_smem_bytes(int b, int W, bool unit, int nt) {
     const size_t xb = W == 256 ? SmemMap<256>{b}.xbytes() : SmemMap<128>{b}.xbytes();
-    return 1024 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
+    return (size_t)W * 8 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
 }
 
 }  // namespace mp

@@ -9,7 +9,7 @@ from paper_1901_10084_b200 import _native, instances  # noqa: E402
 from paper_1901_10084_b200.solver import DeviceSession  # noqa: E402
 
 NAMES = ["pred_wait", "ring_wait", "hot", "cold", "release", "levels", "cold_calls", "-",
-         "prologue", "loop", "epilogue", "prod_busy", "ctas"]
+         "prologue", "loop", "epilogue", "epi_blocks", "ctas", "c_lookup", "c_math", "c_append"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=None)
