@@ -23,6 +23,7 @@
 #include "metricproj_b200.h"
 #include "mp_aux.cuh"
 #include "mp_device.cuh"
+#include "mp_serial.cuh"
 
 using namespace mp;
 
@@ -225,6 +226,23 @@ int enqueue_pass(mp_handle *h) {
     ta.wp = h->pool[wp];
     ta.ctr = h->ctr;
     ta.dbg = getenv("MP_DBG") ? atoi(getenv("MP_DBG")) : 0;
+    if (h->kind == MP_SCHEDULE_SERIAL) {
+        SerialArgs sa{};
+        sa.x = h->x;
+        sa.winvx = h->winvx;
+        sa.ld = h->ld;
+        sa.n = (int32_t)h->n;
+        sa.eps = h->eps;
+        sa.rp = h->pool[h->rp];
+        sa.wp = h->pool[wp];
+        sa.ctr = h->ctr;
+        const int grid = grid_for(h->n * 32, 256, 148 * 8);
+        for (int L = 3; L <= 3 * (int)h->n - 6; ++L) {
+            if (h->unit_x) serial_level_kernel<true><<<grid, 256, 0, h->st>>>(sa, L);
+            else serial_level_kernel<false><<<grid, 256, 0, h->st>>>(sa, L);
+        }
+        CK(cudaGetLastError());
+    }
     for (size_t r = 0; r < h->round_cnt.size(); ++r) {
         if (!h->round_cnt[r]) continue;
         ta.tiles = h->d_tiles + h->round_off[r];
@@ -317,11 +335,12 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     if (!inst->d_flat || !inst->w_flat) return fail(MP_ERR_ARG, "d_flat / w_flat are required");
     if (cfg->schedule_kind < 0 || cfg->schedule_kind > 2)
         return fail(MP_ERR_ARG, "unknown schedule_kind %d", cfg->schedule_kind);
-    if (cfg->schedule_kind == MP_SCHEDULE_SERIAL)
-        return fail(MP_ERR_UNSUPPORTED, "schedule_kind 'serial' is not implemented on the device");
+    if (cfg->schedule_kind == MP_SCHEDULE_SERIAL && n > 8192)
+        return fail(MP_ERR_UNSUPPORTED, "schedule_kind 'serial' is limited to n <= 8192 on the device");
     const int b = cfg->schedule_kind == MP_SCHEDULE_DIAGONAL ? 1 : cfg->tile_b;
     if (b < 1) return fail(MP_ERR_ARG, "tile size must be >= 1, got %d", b);
-    if (b > 48) return fail(MP_ERR_UNSUPPORTED, "tile size %d > 48 is not supported on the device", b);
+    if (b > 48 && cfg->schedule_kind != MP_SCHEDULE_SERIAL)
+        return fail(MP_ERR_UNSUPPORTED, "tile size %d > 48 is not supported on the device", b);
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -402,9 +421,13 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         }
         h->round_cnt.push_back(cnt);
     };
-    for (int64_t z = n - 1; z >= 2; z -= b) emit(1 - b, z);
-    for (int64_t x = 1; x + 2 <= n - 1; x += b) emit(x, n - 1);
-    h->nstreams = (int64_t)h->tiles.size() * nwarps;
+    if (h->kind != MP_SCHEDULE_SERIAL) {
+        for (int64_t z = n - 1; z >= 2; z -= b) emit(1 - b, z);
+        for (int64_t x = 1; x + 2 <= n - 1; x += b) emit(x, n - 1);
+        h->nstreams = (int64_t)h->tiles.size() * nwarps;
+    } else {
+        h->nstreams = 3 * n * n;  // one stream per (level, row), serial_stream()
+    }
     for (const TileDesc &t : h->tiles) {
         const uint64_t keys = (uint64_t)(t.Lend - t.Lbeg + 1) * (uint64_t)h->S * 96ull;
         if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
@@ -491,6 +514,7 @@ int mp_run_passes(mp_handle *h, int32_t npasses, mp_pass_stats *out) {
     h->launches = 0;
     int64_t nlaunch_pass = 2;
     for (int64_t c : h->round_cnt) nlaunch_pass += c ? 1 : 0;
+    if (h->kind == MP_SCHEDULE_SERIAL) nlaunch_pass += 3 * h->n - 8;
     for (int32_t k = 0; k < npasses; ++k) {
         const int wp = h->rp ^ 1;
         // keep the write pool comfortably above the last pass's usage
@@ -612,6 +636,35 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
         double val;
     };
     std::vector<E> ents;
+    if (h->kind == MP_SCHEDULE_SERIAL) {
+        // serial visit order is lexicographic (i, j, k, kind) = ascending key code
+        std::vector<std::pair<int64_t, double>> all;
+        for (int64_t s = 0; s < h->nstreams; ++s) {
+            const int L = (int)(s / n), i = (int)(s % n);
+            int klo, khi;
+            serial_krange((int)n, L, i, klo, khi);
+            if (L < 3 || klo > khi || 3 * i + 3 > L) continue;
+            int32_t c = used ? hh[(size_t)s] : -1;
+            while (c >= 0 && c < used) {
+                for (int e = 0; e < CHUNK; ++e) {
+                    const uint32_t key = hr[(size_t)c].keys[e];
+                    if (key == KEY_END) break;
+                    const int64_t k = klo + key / 3, kind = key % 3, j = L - i - k;
+                    all.push_back({((i * n + j) * n + k) * 3 + kind, hr[(size_t)c].vals[e]});
+                }
+                c = hr[(size_t)c].next;
+            }
+        }
+        std::sort(all.begin(), all.end());
+        if ((int64_t)all.size() != h->nnz)
+            return fail(MP_ERR_CUDA, "dual store inconsistent: %lld vs %lld", (long long)all.size(),
+                        (long long)h->nnz);
+        for (size_t e = 0; e < all.size(); ++e) {
+            if (keys) keys[e] = all[e].first;
+            if (vals) vals[e] = all[e].second;
+        }
+        return MP_OK;
+    }
     for (size_t t = 0; t < h->tiles.size(); ++t) {
         ents.clear();
         const int64_t tx = h->tile_x[t];
@@ -668,6 +721,13 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         if (!(i < j && j < k && k < n)) return fail(MP_ERR_ARG, "invalid metric key %lld", (long long)code);
         if (!(vals[e] > 0.0) || !std::isfinite(vals[e]))
             return fail(MP_ERR_ARG, "dual values must be positive and finite");
+        if (h->kind == MP_SCHEDULE_SERIAL) {
+            const int L = (int)(i + j + k);
+            int klo, khi;
+            serial_krange((int)n, L, (int)i, klo, khi);
+            ents.push_back({serial_stream((int)n, L, (int)i), {(uint32_t)((k - klo) * 3 + kind), vals[e]}});
+            continue;
+        }
         const int64_t iblk = (i + b - 1) / b, kblk = (n - 1 - k) / b;
         if (iblk >= h->nib || kblk >= h->nkb) return fail(MP_ERR_ARG, "key outside schedule");
         const int32_t t = h->tile_of_blk[(size_t)(iblk * h->nkb + kblk)];

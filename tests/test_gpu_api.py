@@ -1,0 +1,161 @@
+"""The reference's solver / acceptance tests (pkg/tests/test_solver.py,
+test_acceptance.py), run against this package's API on the GPU."""
+
+import io
+import json
+
+import numpy as np
+import pytest
+
+from paper_1901_10084_b200 import core, instances, schedule, solver
+from paper_1901_10084_b200.solver import SolverConfig, SolverError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def small_instance():
+    return instances.random_instance(6, seed=123)
+
+
+def test_config_validation():
+    SolverConfig().validate()
+    for bad in (dict(workers=0), dict(tile_size=0), dict(schedule_kind="zigzag"),
+                dict(schedule_kind="serial", workers=2), dict(tol_gap=0.0), dict(fixed_passes=0)):
+        with pytest.raises(ValueError):
+            SolverConfig(**bad).validate()
+
+
+def test_fixed_passes_step_count(small_instance):
+    """test_solver.py:45-53 / acceptance 8: steps = passes * constraint_count."""
+    inst = small_instance
+    expected = core.constraint_count(inst.n)
+    for cfg in (SolverConfig(schedule_kind="serial", fixed_passes=4),
+                SolverConfig(workers=3, tile_size=2, fixed_passes=4)):
+        sol = solver.solve(inst, cfg)
+        assert sol.passes_run == 4 and sol.total_steps == 4 * expected
+    sol = solver.solve(instances.random_instance(15, seed=0), SolverConfig(fixed_passes=20))
+    assert sol.total_steps == 31500
+
+
+def test_results_identical_across_worker_counts():
+    inst = instances.random_instance(11, seed=3)
+    base = solver.solve(inst, SolverConfig(workers=1, tile_size=3, fixed_passes=6))
+    for p in (2, 3, 5):
+        sol = solver.solve(inst, SolverConfig(workers=p, tile_size=3, fixed_passes=6))
+        assert np.array_equal(sol.state.xv, base.state.xv)
+        assert np.array_equal(sol.state.fv, base.state.fv)
+
+
+def test_diagonal_and_tiled_b1_identical():
+    inst = instances.random_instance(9, seed=4)
+    a = solver.solve(inst, SolverConfig(workers=2, schedule_kind="diagonal", fixed_passes=5))
+    b = solver.solve(inst, SolverConfig(workers=2, tile_size=1, fixed_passes=5))
+    assert np.array_equal(a.state.xv, b.state.xv)
+
+
+def test_gap_shrinks_and_stats_consistent(small_instance):
+    sol = solver.solve(small_instance, SolverConfig(fixed_passes=300))
+    gaps = [s.duality_gap for s in sol.stats]
+    assert abs(gaps[-1]) < 1e-6 * max(abs(g) for g in gaps[:10])
+    assert sol.stats[-1].max_violation < 1e-8
+    for s in sol.stats:
+        assert s.duality_gap == pytest.approx(s.primal_objective - s.dual_objective, abs=1e-12)
+        assert s.max_violation >= 0 and s.wall_time >= 0
+
+
+def test_max_violation_reported_matches_state(small_instance):
+    sol = solver.solve(small_instance, SolverConfig(max_passes=2000, tol_gap=1e-6,
+                                                    tol_violation=1e-6))
+    assert sol.converged
+    fresh = core.max_violation(small_instance, sol.state)
+    assert fresh <= sol.stats[-1].max_violation + 1e-12
+
+
+def test_stats_stream(small_instance):
+    buf = io.StringIO()
+    sol = solver.solve(small_instance, SolverConfig(fixed_passes=3), stats_stream=buf)
+    lines = buf.getvalue().splitlines()
+    assert len(lines) == 3 and json.loads(lines[-1])["pass_index"] == 2
+    assert sol.pass_seconds > 0
+
+
+def test_epsilon_override():
+    inst = instances.random_instance(5, seed=8)
+    direct = solver.solve(core.ProblemInstance(5, inst.D, inst.Wt, epsilon=0.9),
+                          SolverConfig(fixed_passes=5))
+    override = solver.solve(inst, SolverConfig(fixed_passes=5, epsilon=0.9))
+    assert np.array_equal(direct.state.xv, override.state.xv)
+    assert np.array_equal(direct.state.fv, override.state.fv)
+
+
+def test_nonfinite_state_raises():
+    inst = instances.random_instance(5, seed=8)
+    plan = solver.Plan(5, SolverConfig())
+    state, duals = solver.initialize(inst)
+    state.xv[0] = np.nan
+    with pytest.raises(SolverError, match="non-finite"):
+        solver.run_pass(state, duals, inst, plan)
+
+
+def test_run_pass_sequence_equals_solve():
+    inst = instances.random_instance(13, seed=5)
+    cfg = SolverConfig(tile_size=4, fixed_passes=6)
+    sol = solver.solve(inst, cfg)
+    plan = solver.Plan(inst.n, cfg)
+    state, duals = solver.initialize(inst, 2)
+    for k in range(6):
+        st = solver.run_pass(state, duals, inst, plan, pass_index=k)
+        assert st.pass_index == k
+    assert np.array_equal(state.xv, sol.state.xv)
+    assert np.array_equal(duals.metric_arrays()[0], sol.duals.metric_arrays()[0])
+    assert core.dual_objective(inst, duals) == pytest.approx(
+        core.dual_objective_from_state(inst, state, duals), rel=1e-10, abs=1e-10)
+
+
+def test_kkt_report_at_convergence(small_instance):
+    """test_solver.py:140-150 / acceptance 7."""
+    inst = small_instance
+    sol = solver.solve(inst, SolverConfig(workers=2, tile_size=2, max_passes=5000, tol_gap=1e-8,
+                                          tol_violation=1e-8))
+    assert sol.converged
+    report = solver.kkt_report(inst, sol.state, sol.duals)
+    assert report["state_relation_residual"] < 1e-10
+    assert report["min_stored_dual"] > 0
+    assert report["max_violation"] <= 1e-8
+    assert report["complementary_slackness"] < 1e-6
+
+
+def test_unique_optimum_across_schedules():
+    """Acceptance 6: every schedule converges to the same optimum."""
+    configs = [dict(schedule_kind="serial"), dict(workers=2, tile_size=2),
+               dict(workers=4, tile_size=5), dict(workers=8, tile_size=8),
+               dict(tile_size=40)]
+    for n in (20, 40):
+        inst = instances.random_instance(n, seed=n)
+        results = []
+        for kw in configs:
+            sol = solver.solve(inst, SolverConfig(max_passes=5000, tol_gap=1e-6,
+                                                  tol_violation=1e-6, **kw))
+            assert sol.converged, (n, kw)
+            results.append(sol.state.X())
+        for other in results[1:]:
+            assert np.max(np.abs(other - results[0])) <= 1e-4
+
+
+def test_worked_example():
+    """Acceptance 4 through a one-pass solve on n=3: x_01=1 violates the
+    triangle; one step moves to (2/3, 1/3, 1/3) with dual eps/3."""
+    eps = 0.7
+    inst = core.ProblemInstance(3, np.zeros((3, 3)), np.ones((3, 3)) - np.eye(3), epsilon=eps)
+    sess = solver.DeviceSession(inst, "serial", 40)
+    xv = np.zeros(3)
+    xv[core.pair_index(3, 0, 1)] = 1.0
+    fv = np.full(3, 1e6)  # large slack: the pair rows stay inactive
+    sess.set_state(xv, fv)
+    sess.run(1)
+    x, _ = sess.state()
+    assert abs(x[core.pair_index(3, 0, 1)] - 2 / 3) <= 1e-15
+    assert abs(x[core.pair_index(3, 0, 2)] - 1 / 3) <= 1e-15
+    keys, vals, _ = sess.duals()
+    assert len(keys) == 1 and abs(vals[0] - eps / 3) <= 1e-15

@@ -148,3 +148,49 @@ def test_session_violation_scan_matches_oracle(oracle_lib):
     sess.run(5)
     x, f = sess.state()
     assert sess.max_violation() == oracle_lib.max_violation(x, f, inst.d_flat, inst.n)
+
+
+@pytest.mark.parametrize("n", [4, 5, 6, 9])
+def test_serial_schedule_bitwise(small_golden, n):
+    """schedule_kind='serial' (_kernels.py:135-183) on the device."""
+    g = small_golden
+    inst = instances.random_instance(n, seed=100 * n)
+    sess = DeviceSession(inst, "serial", 40)
+    sess.run(3)
+    x, f = sess.state()
+    assert np.array_equal(x, g[f"serial_n{n}_x"]) and np.array_equal(f, g[f"serial_n{n}_f"])
+    keys, vals, _ = sess.duals()
+    assert np.array_equal(keys, g[f"serial_n{n}_keys"]) and np.array_equal(vals, g[f"serial_n{n}_vals"])
+    if n <= 6:  # the reference tests' dense Algorithm 1 (tests/reference.py:57-75)
+        assert np.max(np.abs(np.concatenate([x, f]) - g[f"dense_n{n}_v"])) <= 1e-10
+
+
+@pytest.mark.parametrize("n,reg", [(40, False), (77, True), (150, False)])
+def test_serial_against_oracle(oracle_lib, n, reg):
+    inst = instances.config_instance(1, n=n)
+    rx = rf = None
+    if reg:
+        rng = np.random.default_rng(n)
+        rx = rng.uniform(0.5, 2.0, inst.npairs)
+        rf = rng.uniform(0.5, 2.0, inst.npairs)
+        inst.reg_x, inst.reg_f = rx, rf
+    sess = DeviceSession(inst, "serial", 40)
+    ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, reg_x=rx,
+                                  reg_f=rf, kind="serial")
+    for _ in range(5):
+        st = sess.run(1)[0]
+        rs = ref.run_pass()
+        assert st.max_violation == rs.max_violation
+    x, f = sess.state()
+    assert np.array_equal(x, ref.state()[0]) and np.array_equal(f, ref.state()[1])
+    keys, vals, _ = sess.duals()
+    rk, rv = ref.duals()
+    assert np.array_equal(keys, rk) and np.array_equal(vals, rv)
+    # import the oracle's duals and state, continue both: still identical
+    sess2 = DeviceSession(inst, "serial", 40)
+    sess2.set_state(*ref.state())
+    sess2.set_duals(rk, rv, ref.pair_duals())
+    sess2.run(2)
+    ref.run_pass()
+    ref.run_pass()
+    assert np.array_equal(sess2.state()[0], ref.state()[0])
