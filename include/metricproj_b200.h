@@ -141,6 +141,12 @@ void mp_destroy(mp_handle *h);
 int mp_max_violation(int64_t n, const double *xv, const double *fv, const double *d_flat,
                      double *out);
 
+/* Self-test of the device's fast exact division (Markstein step with a
+ * precomputed reciprocal, used for the divisions by eps and by 3 in the metric
+ * step): compares it with IEEE division on `samples` random dividends and
+ * reports the number of results that differ (must be 0). */
+int mp_check_division(double divisor, int64_t samples, uint64_t seed, int64_t *mismatches);
+
 /* Thread-local message for the last error on this thread ("" if none). */
 const char *mp_last_error(void);
 

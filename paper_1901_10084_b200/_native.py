@@ -94,7 +94,8 @@ class MPPassStats(ctypes.Structure):
 # every symbol include/metricproj_b200.h declares
 EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dual_count",
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
-           "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_last_error", "mp_version")
+           "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_check_division",
+           "mp_last_error", "mp_version")
 
 _lib = None
 
@@ -131,6 +132,8 @@ def load():
     L.mp_destroy.restype = None
     L.mp_destroy.argtypes = [P]
     L.mp_max_violation.argtypes = [ctypes.c_int64, D, D, D, D]
+    L.mp_check_division.argtypes = [ctypes.c_double, ctypes.c_int64, ctypes.c_uint64, I]
+    L.mp_check_division.restype = ctypes.c_int
     L.mp_last_error.restype = ctypes.c_char_p
     L.mp_version.restype = ctypes.c_char_p
     for name in ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_get_duals",

@@ -96,6 +96,12 @@ struct PassCounters {
     int32_t pad;
 };
 
+// Divisors of the metric step: eps (always) and s = 3 (W = I).
+struct StepConsts {
+    double eps, reps;  // eps and RN(1/eps); reps = 0 disables the fast path
+    double r3;         // RN(1/3)
+};
+
 struct TileArgs {
     double *x;            // dense n x ld, upper triangle
     const double *winvx;  // dense n x ld, 1/reg_x (general W only)
@@ -108,6 +114,7 @@ struct TileArgs {
     PassCounters *ctr;
     int32_t dbg;  // TEMP experiment switches
     int32_t nwc;  // compute warps per CTA (the rest are ring producers)
+    StepConsts kc;
     unsigned long long *trace;  // optional cycle counters (mp_trace), null = off
 };
 
@@ -141,6 +148,7 @@ struct CtaConst {
     DualPool rp, wp;
     PassCounters *ctr;
     unsigned long long *trace;
+    StepConsts kc;
     int32_t b, nt, xsize, dbg;
 };
 
@@ -150,18 +158,39 @@ struct CtaConst {
 // Divisions whose value is known exactly are skipped: with y = 0,
 // y*s/eps = +0 and delta = d0 (+0), so d0 <= 0 means theta = coef = 0 (no
 // move, nothing stored) -- the same values the reference computes.
+// Correctly rounded a/b from rb = RN(1/b) (Markstein): q0 = RN(a*rb) is
+// within one ulp of a/b, the residual a - q0*b is exact with an FMA, and one
+// correction RN(q0 + r*rb) rounds correctly.  Outside the safe exponent range
+// (or for 0, inf, nan) it falls back to IEEE division; the host only enables
+// it for divisors whose significand is not all ones.  Verified bit for bit
+// against __ddiv_rn by mp_check_division (tests/test_gpu_parity.py).
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+    const double q0 = __dmul_rn(a, rb);
+    const double r = __fma_rn(-q0, b, a);
+    const double q1 = __fma_rn(r, rb, q0);
+    const double aq = fabs(q1);
+    if (!(aq > 0x1p-960 && aq < 0x1p+960)) return __ddiv_rn(a, b);
+    return q1;
+}
+
+
+__device__ __forceinline__ double div_eps(double a, const StepConsts &k) {
+    return k.reps != 0.0 ? div_rn(a, k.eps, k.reps) : __ddiv_rn(a, k.eps);
+}
+
 template <bool UNIT>
 __device__ __forceinline__ double dykstra_row(double &p, double &m1, double &m2, double wp,
-                                              double wm1, double wm2, double y, double eps,
-                                              double &viol) {
+                                              double wm1, double wm2, double y,
+                                              const StepConsts &k, double &viol) {
     const double d0 = __dsub_rn(__dsub_rn(p, m1), m2);
     viol = d0 > viol ? d0 : viol;
     if (y == 0.0 && !(d0 > 0.0)) return 0.0;
     const double s = UNIT ? 3.0 : __dadd_rn(__dadd_rn(wp, wm1), wm2);
-    const double delta = y == 0.0 ? d0 : __dadd_rn(d0, __ddiv_rn(__dmul_rn(y, s), eps));
+    const double delta = y == 0.0 ? d0 : __dadd_rn(d0, div_eps(__dmul_rn(y, s), k));
     double theta = 0.0;
-    if (delta > 0.0) theta = __ddiv_rn(__dmul_rn(eps, delta), s);
-    const double coef = __ddiv_rn(__dsub_rn(y, theta), eps);
+    if (delta > 0.0)
+        theta = UNIT ? div_rn(__dmul_rn(k.eps, delta), 3.0, k.r3) : __ddiv_rn(__dmul_rn(k.eps, delta), s);
+    const double coef = div_eps(__dsub_rn(y, theta), k);
     if (coef != 0.0) {
         if (UNIT) {
             p = __dadd_rn(p, coef);
@@ -499,10 +528,10 @@ __device__ __noinline__ double cold_slot(unsigned char *sm, const CtaConst *cc, 
             wc = ld_sh(pc + xb);
             we = ld_sh(pe + xb);
         }
-        const double eps = cc->eps;
-        t0 = dykstra_row<UNIT>(p, c, e, wa, wc, we, y0, eps, viol);  // IJ: x_ij <= x_ik + x_jk
-        t1 = dykstra_row<UNIT>(c, p, e, wc, wa, we, y1, eps, viol);  // IK: x_ik <= x_ij + x_jk
-        t2 = dykstra_row<UNIT>(e, p, c, we, wa, wc, y2, eps, viol);  // JK: x_jk <= x_ij + x_ik
+        const StepConsts k = cc->kc;
+        t0 = dykstra_row<UNIT>(p, c, e, wa, wc, we, y0, k, viol);  // IJ: x_ij <= x_ik + x_jk
+        t1 = dykstra_row<UNIT>(c, p, e, wc, wa, we, y1, k, viol);  // IK: x_ik <= x_ij + x_jk
+        t2 = dykstra_row<UNIT>(e, p, c, we, wa, wc, y2, k, viol);  // JK: x_jk <= x_ij + x_ik
         st_sh(pa, p);
         st_sh(pc, c);
         st_sh(pe, e);
@@ -931,6 +960,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.xsize = xsize;
         cc.dbg = a.dbg;
         cc.trace = a.trace;
+        cc.kc = a.kc;
     }
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
     if (tid < 32) ts.done[tid] = T.Lbeg - 1;

@@ -24,6 +24,7 @@ struct SerialArgs {
     double eps;
     DualPool rp, wp;
     PassCounters *ctr;
+    StepConsts kc;
 };
 
 // k range of row i at level L: i < j = L-i-k < k <= n-1
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(256) serial_level_kernel(SerialArgs a, int L) 
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int n = a.n;
-    const double eps = a.eps;
+    const StepConsts sk = a.kc;
     double viol = 0.0;
     for (int i = gw; 3 * i + 3 <= L && i <= n - 3; i += nw) {
         int klo, khi;
@@ -113,9 +114,9 @@ __global__ void __launch_bounds__(256) serial_level_kernel(SerialArgs a, int L) 
                         wcc = a.winvx[(int64_t)i * a.ld + k];
                         we = a.winvx[(int64_t)j * a.ld + k];
                     }
-                    t0 = dykstra_row<UNIT>(p, c, e, wa, wcc, we, y0, eps, viol);
-                    t1 = dykstra_row<UNIT>(c, p, e, wcc, wa, we, y1, eps, viol);
-                    t2 = dykstra_row<UNIT>(e, p, c, we, wa, wcc, y2, eps, viol);
+                    t0 = dykstra_row<UNIT>(p, c, e, wa, wcc, we, y0, sk, viol);
+                    t1 = dykstra_row<UNIT>(c, p, e, wcc, wa, we, y1, sk, viol);
+                    t2 = dykstra_row<UNIT>(e, p, c, we, wa, wcc, y2, sk, viol);
                     *pij = p;
                     *pik = c;
                     *pjk = e;

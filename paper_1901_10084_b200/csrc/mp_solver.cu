@@ -86,6 +86,7 @@ struct mp_handle {
     uint32_t flags = 0;
     double eps = 0.0;
     bool unit_x = true, unit_f = true;
+    StepConsts kc{};
 
     // device state (x and winvx dense n x ld; the rest packed C(n,2))
     double *x = nullptr, *winvx = nullptr;
@@ -220,6 +221,7 @@ int enqueue_pass(mp_handle *h) {
     ta.b = h->b;
     ta.nt = h->NT;
     ta.nwc = h->NWC;
+    ta.kc = h->kc;
     ta.trace = h->trace;
     ta.eps = h->eps;
     ta.rp = h->pool[h->rp];
@@ -236,6 +238,7 @@ int enqueue_pass(mp_handle *h) {
         sa.rp = h->pool[h->rp];
         sa.wp = h->pool[wp];
         sa.ctr = h->ctr;
+        sa.kc = h->kc;
         const int grid = grid_for(h->n * 32, 256, 148 * 8);
         for (int L = 3; L <= 3 * (int)h->n - 6; ++L) {
             if (h->unit_x) serial_level_kernel<true><<<grid, 256, 0, h->st>>>(sa, L);
@@ -372,6 +375,15 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     h->flags = cfg->flags;
     h->eps = inst->epsilon;
     const int64_t m = h->m;
+    // fast exact division by eps (div_rn) unless eps's significand is all ones
+    {
+        uint64_t bits;
+        std::memcpy(&bits, &h->eps, sizeof(bits));
+        const bool all_ones = (bits & 0xFFFFFFFFFFFFFull) == 0xFFFFFFFFFFFFFull;
+        h->kc.eps = h->eps;
+        h->kc.reps = (all_ones || getenv("MP_NO_FASTDIV")) ? 0.0 : 1.0 / h->eps;
+        h->kc.r3 = 1.0 / 3.0;
+    }
 
     // regularizer checks (core.py:135-140)
     if (inst->reg_x)
@@ -860,6 +872,46 @@ int mp_flush_l2(mp_handle *h) {
     static unsigned char v = 0;
     CK(cudaMemsetAsync(h->flush, ++v, h->flush_bytes, h->st));
     CK(cudaStreamSynchronize(h->st));
+    return MP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void check_div_kernel(double b, double rb, uint64_t seed, int64_t samples,
+                                 unsigned long long *bad) {
+    unsigned long long nbad = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < samples;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        // splitmix64 -> random double across many binades, both signs
+        uint64_t z = seed + (uint64_t)t * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const int ex = (int)((z >> 52) % 80) - 40;  // |a| in ~[2^-40, 2^40)
+        const double mant = __longlong_as_double((long long)((z & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+        double a = ldexp(mant, ex);
+        if (z & (1ull << 63)) a = -a;
+        if (div_rn(a, b, rb) != __ddiv_rn(a, b)) ++nbad;
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+}  // namespace
+
+extern "C" {
+
+int mp_check_division(double divisor, int64_t samples, uint64_t seed, int64_t *mismatches) {
+    g_err.clear();
+    if (!mismatches || !(divisor > 0.0)) return fail(MP_ERR_ARG, "bad argument");
+    unsigned long long *d = nullptr;
+    CK(cudaMalloc(&d, sizeof(*d)));
+    cudaMemset(d, 0, sizeof(*d));
+    check_div_kernel<<<148 * 8, 256>>>(divisor, 1.0 / divisor, seed, samples, d);
+    unsigned long long hbad = 0;
+    cudaError_t e = cudaMemcpy(&hbad, d, sizeof(hbad), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(MP_ERR_CUDA, "check_division: %s", cudaGetErrorString(e));
+    *mismatches = (int64_t)hbad;
     return MP_OK;
 }
 

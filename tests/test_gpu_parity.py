@@ -194,3 +194,14 @@ def test_serial_against_oracle(oracle_lib, n, reg):
     ref.run_pass()
     ref.run_pass()
     assert np.array_equal(sess2.state()[0], ref.state()[0])
+
+
+@pytest.mark.parametrize("divisor", [0.2, 0.1, 0.7, 0.3, 0.5, 3.0, 1.0 / 7.0, 0.123456789])
+def test_fast_division_is_ieee(divisor):
+    """div_rn (Markstein step with RN(1/b)) equals IEEE division bit for bit."""
+    import ctypes
+    from paper_1901_10084_b200 import _native
+    bad = np.zeros(1, dtype=np.int64)
+    _native.check(_native.load().mp_check_division(divisor, 20_000_000, 12345, _native.iptr(bad)),
+                  "mp_check_division")
+    assert bad[0] == 0
