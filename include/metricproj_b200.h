@@ -135,6 +135,41 @@ int mp_flush_l2(mp_handle *h);
 
 void mp_destroy(mp_handle *h);
 
+/* Like mp_get_duals (metric part only), plus order[e] = schedule index of the
+ * tile entry e belongs to.  On a sharded session it returns that shard's
+ * duals; concatenating every shard's output and stable-sorting it by order
+ * gives the single-worker visit order. */
+int mp_get_duals_ranked(mp_handle *h, int64_t *keys, double *vals, int64_t *order);
+
+/* ---- One instance over several GPUs ------------------------
+ * Replaces the reference's worker threads (solver._worker_pass,
+ * solver.py:116-163; round ownership Round.worker_of, schedule.py:79-80) with
+ * one process per GPU.  The tiles of each round are assigned to ranks by
+ * longest-processing-time (mp_shard_plan); a rank keeps the whole x, runs its
+ * tiles, keeps their duals, and after every round exchanges the pairs its
+ * tiles wrote (NCCL all-gather on the session stream), so every rank follows
+ * the single-GPU trajectory bit for bit.  Counters (nnz, max violation) are
+ * all-reduced, so every rank reports the global PassStats. */
+
+/* Tile owners of the LPT plan, in schedule order (host only, no device).
+ * owner may be NULL to query the tile count. */
+int mp_shard_plan(int64_t n, int32_t b, int32_t world, int32_t *owner, int64_t *ntiles);
+
+/* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
+int mp_nccl_unique_id(void *id);
+
+/* Make a fresh session (before its first pass) rank `rank` of `world`.  With
+ * nccl_id != NULL the ranks are processes joined by an NCCL communicator
+ * (blocks until all ranks call it) and mp_run_passes runs the sharded pass.
+ * With nccl_id == NULL the session is a member of a local group: several
+ * sessions of one process driven together by mp_group_run_passes (exchange by
+ * device copies; a test transport that shares the exact per-round code). */
+int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id);
+
+/* Run npasses over a local group (hs[0..world) = the local shards, any order);
+ * out[] receives the (global) stats, identical on every member. */
+int mp_group_run_passes(mp_handle *const *hs, int32_t world, int32_t npasses, mp_pass_stats *out);
+
 /* Kernel-level drop-in for _kernels.max_violation(xv, fv, dflat, n)
  * (_kernels.py:28-57): host buffers in, exact max violation out.  Runs on the
  * current CUDA device. */

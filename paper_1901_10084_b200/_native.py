@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         nvcc = "/usr/local/cuda/bin/nvcc"
     tmp = out + ".tmp"
     cmd = [nvcc, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-I", CSRC,
-           "-o", tmp, os.path.join(CSRC, "mp_solver.cu")]
+           "-o", tmp, os.path.join(CSRC, "mp_solver.cu"), "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
@@ -95,7 +95,8 @@ class MPPassStats(ctypes.Structure):
 EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dual_count",
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
            "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_check_division",
-           "mp_last_error", "mp_version")
+           "mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
+           "mp_group_run_passes", "mp_last_error", "mp_version")
 
 _lib = None
 
@@ -134,6 +135,16 @@ def load():
     L.mp_max_violation.argtypes = [ctypes.c_int64, D, D, D, D]
     L.mp_check_division.argtypes = [ctypes.c_double, ctypes.c_int64, ctypes.c_uint64, I]
     L.mp_check_division.restype = ctypes.c_int
+    L.mp_get_duals_ranked.argtypes = [P, I, D, I]
+    L.mp_shard_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.POINTER(ctypes.c_int32), I]
+    L.mp_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.mp_shard.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p]
+    L.mp_group_run_passes.argtypes = [ctypes.POINTER(P), ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.POINTER(MPPassStats)]
+    for name in ("mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
+                 "mp_group_run_passes"):
+        getattr(L, name).restype = ctypes.c_int
     L.mp_last_error.restype = ctypes.c_char_p
     L.mp_version.restype = ctypes.c_char_p
     for name in ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_get_duals",

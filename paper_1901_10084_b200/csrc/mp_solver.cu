@@ -10,6 +10,8 @@
 // pinned host memory.  The sparse dual pools are double-buffered: pass k
 // reads the pool pass k-1 wrote (SPEC.md "read pass k-1, write pass k").
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the functions are resolved at run time (nccl_api)
 
 #include <algorithm>
 #include <cmath>
@@ -24,6 +26,7 @@
 #include "mp_aux.cuh"
 #include "mp_device.cuh"
 #include "mp_serial.cuh"
+#include "mp_shard.cuh"
 
 using namespace mp;
 
@@ -40,6 +43,13 @@ int fail(int code, const char *fmt, ...) {
     g_err = buf;
     return code;
 }
+
+#define NCK(call)                                                                     \
+    do {                                                                              \
+        ncclResult_t r_ = (call);                                                     \
+        if (r_ != ncclSuccess)                                                        \
+            return fail(MP_ERR_CUDA, "%s failed: %s", #call, nccl_api().errorString(r_)); \
+    } while (0)
 
 #define CK(call)                                                                        \
     do {                                                                                \
@@ -74,6 +84,107 @@ TileDesc make_tile(int64_t x, int64_t z, int64_t b) {
     t.Lbeg = (int32_t)(t.ilo + j0 + k0);
     t.Lend = (int32_t)(std::min<int64_t>(t.ihi, z - 2) + (z - 1) + z);
     return t;
+}
+
+// Tile bases of a pass in schedule order (schedule.tiled_rounds,
+// schedule.py:117-153): per round the tiles (x + c*b, z - c*b).
+void enumerate_tiles(int64_t n, int64_t b, std::vector<int64_t> &tx, std::vector<int64_t> &tz,
+                     std::vector<int64_t> &round_cnt) {
+    auto emit = [&](int64_t x, int64_t z) {
+        int64_t cnt = 0;
+        for (int64_t c = 0; std::max<int64_t>(x + c * b, 0) + 2 <= z - c * b; ++c) {
+            tx.push_back(x + c * b);
+            tz.push_back(z - c * b);
+            ++cnt;
+        }
+        round_cnt.push_back(cnt);
+    };
+    for (int64_t z = n - 1; z >= 2; z -= b) emit(1 - b, z);
+    for (int64_t x = 1; x + 2 <= n - 1; x += b) emit(x, n - 1);
+}
+
+// Triplets of tile (x, z) (Tile.size, schedule.py:36-67): sum over rows i and
+// columns k >= i+2 of k-i-1.
+int64_t tile_triplets(int64_t x, int64_t z, int64_t b) {
+    const int64_t ilo = std::max<int64_t>(x, 0), ihi = x + b - 1, klo = std::max<int64_t>(z - b + 1, 0);
+    int64_t s = 0;
+    for (int64_t i = ilo; i <= ihi; ++i) {
+        const int64_t a = std::max(klo, i + 2) - i - 1, c = z - i - 1;
+        if (c >= a) s += (a + c) * (c - a + 1) / 2;
+    }
+    return s;
+}
+
+// Longest-processing-time assignment per round (distributed.shard_rounds):
+// tiles by decreasing triplet count (ties: schedule position), each to the
+// least-loaded rank (ties: lowest rank).
+void lpt_owner(int64_t b, int world, const std::vector<int64_t> &tx, const std::vector<int64_t> &tz,
+               const std::vector<int64_t> &round_cnt, std::vector<int32_t> &owner) {
+    owner.assign(tx.size(), 0);
+    int64_t off = 0;
+    for (int64_t cnt : round_cnt) {
+        std::vector<int64_t> idx((size_t)cnt), size((size_t)cnt);
+        for (int64_t t = 0; t < cnt; ++t) {
+            idx[(size_t)t] = t;
+            size[(size_t)t] = tile_triplets(tx[(size_t)(off + t)], tz[(size_t)(off + t)], b);
+        }
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int64_t a, int64_t c) { return size[(size_t)a] > size[(size_t)c]; });
+        std::vector<int64_t> load((size_t)world, 0);
+        for (int64_t t : idx) {
+            int g = 0;
+            for (int r = 1; r < world; ++r)
+                if (load[(size_t)r] < load[(size_t)g]) g = r;
+            owner[(size_t)(off + t)] = g;
+            load[(size_t)g] += size[(size_t)t];
+        }
+        off += cnt;
+    }
+}
+
+// NCCL, resolved at run time so the library loads (and the CPU tests run)
+// without it: prefer the copy already in the process (torch's), then
+// $MP_NCCL_LIB, then the system libnccl.so.2.
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                              ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char *(*errorString)(ncclResult_t) = nullptr;
+    std::string why;
+};
+
+const NcclApi &nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib && getenv("MP_NCCL_LIB")) lib = dlopen(getenv("MP_NCCL_LIB"), RTLD_NOW);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW);
+        if (!lib) {
+            a.why = dlerror() ? dlerror() : "dlopen(libnccl.so.2) failed";
+            return a;
+        }
+        a.getUniqueId = (decltype(a.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+        a.commInitRank = (decltype(a.commInitRank))dlsym(lib, "ncclCommInitRank");
+        a.commDestroy = (decltype(a.commDestroy))dlsym(lib, "ncclCommDestroy");
+        a.allGather = (decltype(a.allGather))dlsym(lib, "ncclAllGather");
+        a.allReduce = (decltype(a.allReduce))dlsym(lib, "ncclAllReduce");
+        a.groupStart = (decltype(a.groupStart))dlsym(lib, "ncclGroupStart");
+        a.groupEnd = (decltype(a.groupEnd))dlsym(lib, "ncclGroupEnd");
+        a.errorString = (decltype(a.errorString))dlsym(lib, "ncclGetErrorString");
+        if (!a.getUniqueId || !a.commInitRank || !a.commDestroy || !a.allGather || !a.allReduce ||
+            !a.groupStart || !a.groupEnd || !a.errorString) {
+            a.why = "libnccl.so.2 lacks a required symbol";
+            a.getUniqueId = nullptr;
+        }
+        return a;
+    }();
+    return api;
 }
 
 }  // namespace
@@ -125,6 +236,21 @@ struct mp_handle {
     void *flush = nullptr;
     size_t flush_bytes = 0;
 
+    // sharded execution (mp_shard; mp_shard.cuh)
+    struct Shard {
+        int world = 1, rank = 0;
+        bool on = false, local = false;  // local: test transport (mp_group_run_passes)
+        ncclComm_t comm = nullptr;
+        std::vector<int32_t> owner;               // per tile
+        std::vector<int64_t> my_off, my_cnt;      // per round, into d_my_tiles
+        std::vector<int64_t> round_max;           // per round: max footprint values over ranks
+        TileDesc *d_my_tiles = nullptr;
+        FootDesc *d_foot = nullptr;               // per tile, schedule order
+        double *sendbuf = nullptr, *recvbuf = nullptr;
+        PassCounters *d_local = nullptr, *h_local = nullptr;  // this rank's counters
+        int64_t local_nnz = 0;
+    } sh;
+
     ~mp_handle() {
         if (dev >= 0) cudaSetDevice(dev);
         double *bufs[] = {x, winvx, f, d, w, regx, regf, winvf, pu, pl, tmp,
@@ -144,6 +270,13 @@ struct mp_handle {
         if (h_stats) cudaFreeHost(h_stats);
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
+        cudaFree(sh.d_my_tiles);
+        cudaFree(sh.d_foot);
+        cudaFree(sh.sendbuf);
+        cudaFree(sh.recvbuf);
+        cudaFree(sh.d_local);
+        if (sh.h_local) cudaFreeHost(sh.h_local);
+        if (sh.comm) nccl_api().commDestroy(sh.comm);
         if (st) cudaStreamDestroy(st);
     }
 };
@@ -203,17 +336,7 @@ int launch_pairs(mp_handle *h, const PairArgs &a) {
     return MP_OK;
 }
 
-// Enqueue one pass (no host sync).  Returns an MP_* code for launch errors.
-int enqueue_pass(mp_handle *h) {
-    const int wp = h->rp ^ 1;
-    CK(cudaMemsetAsync(h->ctr, 0, sizeof(PassCounters), h->st));
-    // snapshot for an overflow retry of this pass
-    CK(cudaMemcpyAsync(h->snap_x, h->x, (size_t)h->n * h->ld * sizeof(double),
-                       cudaMemcpyDeviceToDevice, h->st));
-    CK(cudaMemcpyAsync(h->snap_f, h->f, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
-    CK(cudaMemcpyAsync(h->snap_pu, h->pu, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
-    CK(cudaMemcpyAsync(h->snap_pl, h->pl, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
-    CK(cudaEventRecord(h->ev[1], h->st));
+TileArgs tile_args(mp_handle *h) {
     TileArgs ta{};
     ta.x = h->x;
     ta.winvx = h->winvx;
@@ -225,33 +348,80 @@ int enqueue_pass(mp_handle *h) {
     ta.trace = h->trace;
     ta.eps = h->eps;
     ta.rp = h->pool[h->rp];
-    ta.wp = h->pool[wp];
+    ta.wp = h->pool[h->rp ^ 1];
     ta.ctr = h->ctr;
     ta.dbg = getenv("MP_DBG") ? atoi(getenv("MP_DBG")) : 0;
-    if (h->kind == MP_SCHEDULE_SERIAL) {
-        SerialArgs sa{};
-        sa.x = h->x;
-        sa.winvx = h->winvx;
-        sa.ld = h->ld;
-        sa.n = (int32_t)h->n;
-        sa.eps = h->eps;
-        sa.rp = h->pool[h->rp];
-        sa.wp = h->pool[wp];
-        sa.ctr = h->ctr;
-        sa.kc = h->kc;
-        const int grid = grid_for(h->n * 32, 256, 148 * 8);
-        for (int L = 3; L <= 3 * (int)h->n - 6; ++L) {
-            if (h->unit_x) serial_level_kernel<true><<<grid, 256, 0, h->st>>>(sa, L);
-            else serial_level_kernel<false><<<grid, 256, 0, h->st>>>(sa, L);
-        }
-        CK(cudaGetLastError());
+    return ta;
+}
+
+// Pass = begin, [serial levels | rounds (+ exchange when sharded)],
+// [counter all-reduce when sharded], end.  Nothing here syncs the host.
+int pass_begin(mp_handle *h) {
+    CK(cudaMemsetAsync(h->ctr, 0, sizeof(PassCounters), h->st));
+    // snapshot for an overflow retry of this pass
+    CK(cudaMemcpyAsync(h->snap_x, h->x, (size_t)h->n * h->ld * sizeof(double),
+                       cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->snap_f, h->f, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->snap_pu, h->pu, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->snap_pl, h->pl, h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaEventRecord(h->ev[1], h->st));
+    return MP_OK;
+}
+
+int pass_serial(mp_handle *h) {
+    SerialArgs sa{};
+    sa.x = h->x;
+    sa.winvx = h->winvx;
+    sa.ld = h->ld;
+    sa.n = (int32_t)h->n;
+    sa.eps = h->eps;
+    sa.rp = h->pool[h->rp];
+    sa.wp = h->pool[h->rp ^ 1];
+    sa.ctr = h->ctr;
+    sa.kc = h->kc;
+    const int grid = grid_for(h->n * 32, 256, 148 * 8);
+    for (int L = 3; L <= 3 * (int)h->n - 6; ++L) {
+        if (h->unit_x) serial_level_kernel<true><<<grid, 256, 0, h->st>>>(sa, L);
+        else serial_level_kernel<false><<<grid, 256, 0, h->st>>>(sa, L);
     }
-    for (size_t r = 0; r < h->round_cnt.size(); ++r) {
-        if (!h->round_cnt[r]) continue;
-        ta.tiles = h->d_tiles + h->round_off[r];
-        int rc = launch_tiles(h, ta, (int)h->round_cnt[r]);
-        if (rc) return rc;
-    }
+    CK(cudaGetLastError());
+    return MP_OK;
+}
+
+// This rank's tiles of round r: one CTA per tile.
+int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
+    const int64_t cnt = h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r];
+    if (!cnt) return MP_OK;
+    ta.tiles = h->sh.on ? h->sh.d_my_tiles + h->sh.my_off[r] : h->d_tiles + h->round_off[r];
+    return launch_tiles(h, ta, (int)cnt);
+}
+
+bool round_exchanges(const mp_handle *h, size_t r) {
+    return h->sh.on && h->sh.world > 1 && h->round_cnt[r] > 0 && h->sh.round_max[r] > 0;
+}
+
+int pass_pack(mp_handle *h, size_t r) {
+    foot_copy_kernel<true><<<(unsigned)h->round_cnt[r], 256, 0, h->st>>>(
+        h->sh.d_foot + h->round_off[r], h->x, h->ld, h->b, h->sh.sendbuf, 0, h->sh.rank);
+    CK(cudaGetLastError());
+    return MP_OK;
+}
+
+int pass_unpack(mp_handle *h, size_t r) {
+    foot_copy_kernel<false><<<(unsigned)h->round_cnt[r], 256, 0, h->st>>>(
+        h->sh.d_foot + h->round_off[r], h->x, h->ld, h->b, h->sh.recvbuf, h->sh.round_max[r],
+        h->sh.rank);
+    CK(cudaGetLastError());
+    return MP_OK;
+}
+
+// Keep this rank's own counters (its duals) before the all-reduce.
+int pass_keep_local(mp_handle *h) {
+    CK(cudaMemcpyAsync(h->sh.d_local, h->ctr, sizeof(PassCounters), cudaMemcpyDeviceToDevice, h->st));
+    return MP_OK;
+}
+
+int pass_end(mp_handle *h) {
     CK(cudaEventRecord(h->ev[2], h->st));
     PairArgs pa{};
     pa.x = h->x;
@@ -276,6 +446,79 @@ int enqueue_pass(mp_handle *h) {
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev[3], h->st));
     CK(cudaMemcpyAsync(h->h_stats, h->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, h->st));
+    if (h->sh.on)
+        CK(cudaMemcpyAsync(h->sh.h_local, h->sh.d_local, sizeof(PassCounters), cudaMemcpyDeviceToHost,
+                           h->st));
+    return MP_OK;
+}
+
+// Enqueue one pass of a group of sessions that solve one instance together:
+// a single unsharded session, one NCCL rank (hs = {this rank}), or all ranks
+// of a local group sharing one stream (test transport).
+int enqueue_group_pass(std::vector<mp_handle *> &hs, PassCounters **d_ctrs) {
+    mp_handle *h0 = hs[0];
+    for (mp_handle *h : hs) {
+        CK(cudaEventRecord(h->ev[0], h->st));
+        int rc = pass_begin(h);
+        if (rc) return rc;
+    }
+    if (h0->kind == MP_SCHEDULE_SERIAL) {
+        int rc = pass_serial(h0);
+        if (rc) return rc;
+    }
+    std::vector<TileArgs> ta;
+    for (mp_handle *h : hs) ta.push_back(tile_args(h));
+    for (size_t r = 0; r < h0->round_cnt.size(); ++r) {
+        for (size_t g = 0; g < hs.size(); ++g) {
+            int rc = pass_round(hs[g], r, ta[g]);
+            if (rc) return rc;
+        }
+        if (!round_exchanges(h0, r)) continue;
+        for (mp_handle *h : hs) {
+            int rc = pass_pack(h, r);
+            if (rc) return rc;
+        }
+        const int64_t cnt = h0->sh.round_max[r];
+        if (h0->sh.local) {
+            for (mp_handle *dst : hs)
+                for (mp_handle *src : hs)
+                    if (src != dst)
+                        CK(cudaMemcpyAsync(dst->sh.recvbuf + (int64_t)src->sh.rank * cnt, src->sh.sendbuf,
+                                           (size_t)cnt * sizeof(double), cudaMemcpyDeviceToDevice,
+                                           h0->st));
+        } else {
+            NCK(nccl_api().allGather(h0->sh.sendbuf, h0->sh.recvbuf, (size_t)cnt, ncclFloat64,
+                                     h0->sh.comm, h0->st));
+        }
+        for (mp_handle *h : hs) {
+            int rc = pass_unpack(h, r);
+            if (rc) return rc;
+        }
+    }
+    if (h0->sh.on) {
+        for (mp_handle *h : hs) {
+            int rc = pass_keep_local(h);
+            if (rc) return rc;
+        }
+        if (h0->sh.world > 1) {
+            if (h0->sh.local) {
+                reduce_counters_kernel<<<1, 32, 0, h0->st>>>(d_ctrs, (int)hs.size());
+                CK(cudaGetLastError());
+            } else {
+                const NcclApi &N = nccl_api();
+                PassCounters *c = h0->ctr;
+                NCK(N.groupStart());
+                NCK(N.allReduce(&c->viol_bits, &c->viol_bits, 1, ncclUint64, ncclMax, h0->sh.comm, h0->st));
+                NCK(N.allReduce(&c->nnz, &c->nnz, 1, ncclUint64, ncclSum, h0->sh.comm, h0->st));
+                NCK(N.allReduce(&c->overflow, &c->overflow, 1, ncclInt32, ncclMax, h0->sh.comm, h0->st));
+                NCK(N.groupEnd());
+            }
+        }
+    }
+    for (mp_handle *h : hs) {
+        int rc = pass_end(h);
+        if (rc) return rc;
+    }
     return MP_OK;
 }
 
@@ -518,69 +761,118 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
 
 void mp_destroy(mp_handle *h) { delete h; }
 
-int mp_run_passes(mp_handle *h, int32_t npasses, mp_pass_stats *out) {
-    g_err.clear();
-    if (!h || npasses < 0 || (npasses > 0 && !out)) return fail(MP_ERR_ARG, "bad argument");
-    CK(cudaSetDevice(h->dev));
-    h->metric_ms = h->pair_ms = 0.0;
-    h->launches = 0;
-    int64_t nlaunch_pass = 2;
-    for (int64_t c : h->round_cnt) nlaunch_pass += c ? 1 : 0;
-    if (h->kind == MP_SCHEDULE_SERIAL) nlaunch_pass += 3 * h->n - 8;
+}  // extern "C"
+
+namespace {
+
+// Kernels one session launches per pass (its own, not library calls).
+int64_t launches_per_pass(const mp_handle *h) {
+    int64_t c = 2;  // pair phase + finalize
+    for (size_t r = 0; r < h->round_cnt.size(); ++r) {
+        c += (h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r]) ? 1 : 0;
+        if (round_exchanges(h, r)) c += 2;  // pack + unpack
+    }
+    if (h->kind == MP_SCHEDULE_SERIAL) c += 3 * h->n - 8;
+    if (h->sh.on && h->sh.local && h->sh.world > 1 && h->sh.rank == 0) c += 1;  // counter reduce
+    return c;
+}
+
+// run_pass x npasses (solver.py:166-210) for a group of sessions solving one
+// instance together (see enqueue_group_pass); stats come from hs[0].
+int run_group(std::vector<mp_handle *> &hs, int32_t npasses, mp_pass_stats *out) {
+    mp_handle *h0 = hs[0];
+    for (mp_handle *h : hs) {
+        h->metric_ms = h->pair_ms = 0.0;
+        h->launches = 0;
+    }
+    PassCounters **d_ctrs = nullptr;
+    if (hs.size() > 1) {
+        std::vector<PassCounters *> ptrs;
+        for (mp_handle *h : hs) ptrs.push_back(h->ctr);
+        CK(cudaMalloc(&d_ctrs, ptrs.size() * sizeof(PassCounters *)));
+        CK(cudaMemcpy(d_ctrs, ptrs.data(), ptrs.size() * sizeof(PassCounters *), cudaMemcpyHostToDevice));
+    }
+    struct Free {
+        PassCounters **p;
+        ~Free() { cudaFree(p); }
+    } free_ctrs{d_ctrs};
+    auto local_chunks = [](const mp_handle *h) {
+        return h->sh.on ? h->sh.h_local->chunks_used : h->h_stats->chunks_used;
+    };
     for (int32_t k = 0; k < npasses; ++k) {
-        const int wp = h->rp ^ 1;
-        // keep the write pool comfortably above the last pass's usage
-        const int64_t want = std::max<int64_t>(h->pool[wp].cap, 2 * (int64_t)h->pool_used[h->rp] + 1024);
-        if (want > h->pool[wp].cap) {
-            CK(cudaStreamSynchronize(h->st));
-            int rc = alloc_pool(h, wp, (int32_t)std::min<int64_t>(want, 0x7fffffff));
-            if (rc) return rc;
+        const int wp = h0->rp ^ 1;
+        for (mp_handle *h : hs) {
+            // keep the write pool comfortably above the last pass's usage
+            const int64_t want = std::max<int64_t>(h->pool[wp].cap, 2 * (int64_t)h->pool_used[h->rp] + 1024);
+            if (want > h->pool[wp].cap) {
+                CK(cudaStreamSynchronize(h->st));
+                int rc = alloc_pool(h, wp, (int32_t)std::min<int64_t>(want, 0x7fffffff));
+                if (rc) return rc;
+            }
         }
         for (int attempt = 0;; ++attempt) {
-            CK(cudaEventRecord(h->ev[0], h->st));
-            int rc = enqueue_pass(h);
+            int rc = enqueue_group_pass(hs, d_ctrs);
             if (rc) return rc;
-            CK(cudaStreamSynchronize(h->st));
-            if (!h->h_stats->overflow) break;
-            // dual pool overflow: roll the pass back, grow the pool, redo it
-            rc = restore_snapshot(h);
-            if (rc) return rc;
-            CK(cudaStreamSynchronize(h->st));
-            const int64_t grow = std::max<int64_t>(2 * (int64_t)h->pool[wp].cap,
-                                                   (int64_t)h->h_stats->chunks_used * 2);
-            if (attempt > 8 || grow > 0x7fffffff)
-                return fail(MP_ERR_OOM, "dual pool cannot grow further");
-            rc = alloc_pool(h, wp, (int32_t)grow);
-            if (rc) return rc;
+            for (mp_handle *h : hs) CK(cudaStreamSynchronize(h->st));
+            if (!h0->h_stats->overflow) break;  // all-reduced: every rank agrees
+            // dual pool overflow: roll the pass back, grow the pools, redo it
+            for (mp_handle *h : hs) {
+                rc = restore_snapshot(h);
+                if (rc) return rc;
+                CK(cudaStreamSynchronize(h->st));
+                const int64_t grow = std::max<int64_t>(2 * (int64_t)h->pool[wp].cap,
+                                                       (int64_t)local_chunks(h) * 2);
+                if (attempt > 8 || grow > 0x7fffffff)
+                    return fail(MP_ERR_OOM, "dual pool cannot grow further");
+                rc = alloc_pool(h, wp, (int32_t)grow);
+                if (rc) return rc;
+            }
         }
-        // device time of the pass (snapshot .. finalize), metric vs pair phase
-        float ms_all = 0.f, ms_metric = 0.f, ms_pair = 0.f;
-        CK(cudaEventElapsedTime(&ms_all, h->ev[0], h->ev[3]));
-        CK(cudaEventElapsedTime(&ms_metric, h->ev[1], h->ev[2]));
-        CK(cudaEventElapsedTime(&ms_pair, h->ev[2], h->ev[3]));
-        h->metric_ms += ms_metric;
-        h->pair_ms += ms_pair;
-        h->launches += nlaunch_pass;
-        const DevStats &s = *h->h_stats;
+        for (mp_handle *h : hs) {
+            // device time of the pass (snapshot .. finalize), metric vs pair phase
+            float ms_metric = 0.f, ms_pair = 0.f;
+            CK(cudaEventElapsedTime(&ms_metric, h->ev[1], h->ev[2]));
+            CK(cudaEventElapsedTime(&ms_pair, h->ev[2], h->ev[3]));
+            h->metric_ms += ms_metric;
+            h->pair_ms += ms_pair;
+            h->launches += launches_per_pass(h);
+            h->pool_used[wp] = local_chunks(h);
+            h->rp = wp;
+            h->nnz = h->sh.on ? (int64_t)h->sh.h_local->nnz : (int64_t)h->h_stats->nnz;
+            h->pass_index++;
+        }
+        float ms_all = 0.f;
+        CK(cudaEventElapsedTime(&ms_all, h0->ev[0], h0->ev[3]));
+        const DevStats &s = *h0->h_stats;
         mp_pass_stats &o = out[k];
-        o.pass_index = h->pass_index;
-        o.steps = 3 * (h->n * (h->n - 1) * (h->n - 2) / 6) + 2 * h->m;
+        o.pass_index = h0->pass_index - 1;
+        o.steps = 3 * (h0->n * (h0->n - 1) * (h0->n - 2) / 6) + 2 * h0->m;
         o.nnz_metric = (int64_t)s.nnz;
         o.primal_objective = s.primal;
         o.dual_objective = s.dual;
         o.duality_gap = s.gap;
         o.max_violation = s.viol;
         o.wall_time = ms_all * 1e-3;
-        h->pool_used[wp] = s.chunks_used;
-        h->rp = wp;
-        h->nnz = (int64_t)s.nnz;
-        h->pass_index++;
         if (s.nonfinite) {
             return fail(MP_ERR_NONFINITE, "non-finite value in state after pass %lld",
                         (long long)o.pass_index);
         }
     }
     return MP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mp_run_passes(mp_handle *h, int32_t npasses, mp_pass_stats *out) {
+    g_err.clear();
+    if (!h || npasses < 0 || (npasses > 0 && !out)) return fail(MP_ERR_ARG, "bad argument");
+    if (h->sh.on && h->sh.local && h->sh.world > 1)
+        return fail(MP_ERR_ARG, "a local-transport shard runs only through mp_group_run_passes");
+    CK(cudaSetDevice(h->dev));
+    std::vector<mp_handle *> hs{h};
+    return run_group(hs, npasses, out);
 }
 
 int mp_get_state(mp_handle *h, double *xv, double *fv) {
@@ -615,7 +907,14 @@ int mp_set_state(mp_handle *h, const double *xv, const double *fv) {
 
 int64_t mp_dual_count(mp_handle *h) { return h ? h->nnz : -1; }
 
-int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) {
+}  // extern "C"
+
+namespace {
+
+// Duals of this session in the reference's single-worker visit order; order[e]
+// (optional) = schedule index of the entry's tile, so the shards of a sharded
+// solve merge into the global order with a stable sort on it.
+int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals, int64_t *order) {
     g_err.clear();
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
@@ -674,6 +973,7 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
         for (size_t e = 0; e < all.size(); ++e) {
             if (keys) keys[e] = all[e].first;
             if (vals) vals[e] = all[e].second;
+            if (order) order[e] = (int64_t)e;
         }
         return MP_OK;
     }
@@ -708,12 +1008,25 @@ int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) 
             if (outpos >= h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent (count)");
             if (keys) keys[outpos] = en.key;
             if (vals) vals[outpos] = en.val;
+            if (order) order[outpos] = (int64_t)t;
             ++outpos;
         }
     }
     if (outpos != h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent: %lld vs %lld",
                                       (long long)outpos, (long long)h->nnz);
     return MP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mp_get_duals(mp_handle *h, int64_t *keys, double *vals, double *pair_duals) {
+    return get_duals_impl(h, keys, vals, pair_duals, nullptr);
+}
+
+int mp_get_duals_ranked(mp_handle *h, int64_t *keys, double *vals, int64_t *order) {
+    return get_duals_impl(h, keys, vals, nullptr, order);
 }
 
 int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *vals,
@@ -744,6 +1057,7 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         if (iblk >= h->nib || kblk >= h->nkb) return fail(MP_ERR_ARG, "key outside schedule");
         const int32_t t = h->tile_of_blk[(size_t)(iblk * h->nkb + kblk)];
         if (t < 0) return fail(MP_ERR_ARG, "key outside schedule");
+        if (h->sh.on && h->sh.owner[(size_t)t] != h->sh.rank) continue;  // another shard's dual
         const TileDesc &T = h->tiles[(size_t)t];
         const int64_t q = (i - T.ilo) * b + (k - T.klo);
         const int64_t w = q / (32 * h->S), s = (q % (32 * h->S)) / 32, lane = q % 32;
@@ -796,7 +1110,7 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         CK(cudaMemcpyAsync(P.head, hh.data(), hh.size() * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
     CK(cudaStreamSynchronize(h->st));
     h->pool_used[rp] = used;
-    h->nnz = nnz;
+    h->nnz = (int64_t)ents.size();
     if (pair_duals) {
         std::vector<double> a((size_t)h->m), c((size_t)h->m);
         for (int64_t p = 0; p < h->m; ++p) {
@@ -873,6 +1187,130 @@ int mp_flush_l2(mp_handle *h) {
     CK(cudaMemsetAsync(h->flush, ++v, h->flush_bytes, h->st));
     CK(cudaStreamSynchronize(h->st));
     return MP_OK;
+}
+
+// ---- sharded execution (mp_shard.cuh) -----------------------
+
+int mp_shard_plan(int64_t n, int32_t b, int32_t world, int32_t *owner, int64_t *ntiles) {
+    g_err.clear();
+    if (n < 3 || b < 1 || world < 1 || !ntiles) return fail(MP_ERR_ARG, "bad argument");
+    std::vector<int64_t> tx, tz, rc;
+    enumerate_tiles(n, b, tx, tz, rc);
+    *ntiles = (int64_t)tx.size();
+    if (owner) {
+        std::vector<int32_t> o;
+        lpt_owner(b, world, tx, tz, rc, o);
+        std::copy(o.begin(), o.end(), owner);
+    }
+    return MP_OK;
+}
+
+int mp_nccl_unique_id(void *id) {
+    g_err.clear();
+    if (!id) return fail(MP_ERR_ARG, "null argument");
+    const NcclApi &N = nccl_api();
+    if (!N.getUniqueId) return fail(MP_ERR_UNSUPPORTED, "NCCL unavailable: %s", N.why.c_str());
+    ncclUniqueId u;
+    NCK(N.getUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+    return MP_OK;
+}
+
+int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id) {
+    g_err.clear();
+    if (!h || world < 1 || rank < 0 || rank >= world) return fail(MP_ERR_ARG, "bad argument");
+    if (h->sh.on) return fail(MP_ERR_ARG, "session is already sharded");
+    if (h->kind == MP_SCHEDULE_SERIAL)
+        return fail(MP_ERR_UNSUPPORTED, "sharding needs the tiled or diagonal schedule");
+    if (h->pass_index != 0 || h->nnz != 0) return fail(MP_ERR_ARG, "shard a session before its first pass");
+    CK(cudaSetDevice(h->dev));
+    auto &S = h->sh;
+    std::vector<int64_t> tz;
+    for (const TileDesc &t : h->tiles) tz.push_back(t.z);
+    lpt_owner(h->b, world, h->tile_x, tz, h->round_cnt, S.owner);
+    std::vector<TileDesc> mine;
+    std::vector<FootDesc> foot(h->tiles.size());
+    S.my_off.clear();
+    S.my_cnt.clear();
+    S.round_max.clear();
+    int64_t maxbuf = 0;
+    for (size_t r = 0; r < h->round_cnt.size(); ++r) {
+        std::vector<int64_t> used((size_t)world, 0);
+        S.my_off.push_back((int64_t)mine.size());
+        int64_t cnt = 0;
+        for (int64_t t = h->round_off[r]; t < h->round_off[r] + h->round_cnt[r]; ++t) {
+            const TileDesc &T = h->tiles[(size_t)t];
+            FootDesc f{};
+            f.t = T;
+            f.wr0 = std::max(T.jlo, T.ilo + 1);
+            f.wrw = std::max(0, std::min(T.jhi, T.klo - 1) - f.wr0 + 1);
+            f.wk0 = std::max(T.jlo, T.ihi + 1);
+            f.nwk = std::max(0, T.jhi - f.wk0 + 1);
+            f.owner = S.owner[(size_t)t];
+            f.off = used[(size_t)f.owner];
+            used[(size_t)f.owner] += foot_count(f, h->b);
+            foot[(size_t)t] = f;
+            if (f.owner == rank) {
+                mine.push_back(T);
+                ++cnt;
+            }
+        }
+        S.my_cnt.push_back(cnt);
+        S.round_max.push_back(*std::max_element(used.begin(), used.end()));
+        maxbuf = std::max(maxbuf, S.round_max.back());
+    }
+    CK(cudaMalloc(&S.d_my_tiles, std::max<size_t>(mine.size(), 1) * sizeof(TileDesc)));
+    if (!mine.empty())
+        CK(cudaMemcpy(S.d_my_tiles, mine.data(), mine.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&S.d_foot, std::max<size_t>(foot.size(), 1) * sizeof(FootDesc)));
+    if (!foot.empty())
+        CK(cudaMemcpy(S.d_foot, foot.data(), foot.size() * sizeof(FootDesc), cudaMemcpyHostToDevice));
+    if (world > 1) {
+        CK(cudaMalloc(&S.sendbuf, (size_t)std::max<int64_t>(maxbuf, 1) * sizeof(double)));
+        CK(cudaMalloc(&S.recvbuf, (size_t)std::max<int64_t>(maxbuf, 1) * world * sizeof(double)));
+    }
+    CK(cudaMalloc(&S.d_local, sizeof(PassCounters)));
+    CK(cudaMallocHost(&S.h_local, sizeof(PassCounters)));
+    std::memset(S.h_local, 0, sizeof(PassCounters));
+    S.world = world;
+    S.rank = rank;
+    S.local = nccl_id == nullptr;
+    if (nccl_id) {  // (a 1-rank communicator too: exercises the same set-up)
+        const NcclApi &N = nccl_api();
+        if (!N.commInitRank) return fail(MP_ERR_UNSUPPORTED, "NCCL unavailable: %s", N.why.c_str());
+        ncclUniqueId u;
+        std::memcpy(&u, nccl_id, sizeof(u));
+        NCK(N.commInitRank(&S.comm, world, u, rank));
+    }
+    S.on = true;
+    return MP_OK;
+}
+
+int mp_group_run_passes(mp_handle *const *hs, int32_t world, int32_t npasses, mp_pass_stats *out) {
+    g_err.clear();
+    if (!hs || world < 1 || npasses < 0 || (npasses > 0 && !out)) return fail(MP_ERR_ARG, "bad argument");
+    std::vector<mp_handle *> v((size_t)world, nullptr);
+    for (int32_t g = 0; g < world; ++g) {
+        mp_handle *h = hs[g];
+        if (!h || !h->sh.on || !h->sh.local || h->sh.world != world)
+            return fail(MP_ERR_ARG, "member %d is not a local shard of a %d-way group", g, world);
+        if (v[(size_t)h->sh.rank]) return fail(MP_ERR_ARG, "rank %d appears twice", h->sh.rank);
+        if (h->dev != hs[0]->dev || h->n != hs[0]->n || h->b != hs[0]->b ||
+            h->pass_index != hs[0]->pass_index)
+            return fail(MP_ERR_ARG, "group members differ in device, instance size, tile size or pass");
+        v[(size_t)h->sh.rank] = h;
+    }
+    CK(cudaSetDevice(v[0]->dev));
+    // one stream for the whole group: the members' kernels run one after the
+    // other, none waits on another
+    std::vector<cudaStream_t> own;
+    for (mp_handle *h : v) {
+        own.push_back(h->st);
+        h->st = v[0]->st;
+    }
+    const int rc = run_group(v, npasses, out);
+    for (size_t g = 0; g < v.size(); ++g) v[g]->st = own[g];
+    return rc;
 }
 
 }  // extern "C"

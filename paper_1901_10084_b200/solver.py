@@ -164,6 +164,30 @@ class DeviceSession:
         _native.check(rc, "mp_set_duals")
         self.version += 1
 
+    def shard(self, world, rank, nccl_id=None):
+        """Make this fresh session rank ``rank`` of ``world`` (mp_shard): with
+        a 128-byte NCCL id the ranks are processes, without one the session is
+        a member of a distributed.LocalShardGroup."""
+        rc = _native.load().mp_shard(self._h, int(world), int(rank),
+                                     None if nccl_id is None else bytes(nccl_id))
+        if rc == _native.MP_ERR_ARG:
+            raise ValueError(_native.last_error())
+        if rc == _native.MP_ERR_UNSUPPORTED:
+            raise NotImplementedError(_native.last_error())
+        _native.check(rc, "mp_shard")
+
+    def duals_ranked(self):
+        """(keys, vals, order): this session's metric duals in visit order and
+        the schedule index of each entry's tile (mp_get_duals_ranked)."""
+        c = self.dual_count()
+        keys = np.empty(c, dtype=np.int64)
+        vals = np.empty(c)
+        order = np.empty(c, dtype=np.int64)
+        _native.check(_native.load().mp_get_duals_ranked(self._h, _native.iptr(keys),
+                                                         _native.dptr(vals), _native.iptr(order)),
+                      "mp_get_duals_ranked")
+        return keys, vals, order
+
     def max_violation(self):
         out = np.zeros(1)
         _native.check(_native.load().mp_state_max_violation(self._h, _native.dptr(out)),

@@ -67,3 +67,155 @@ def test_gloo_two_ranks_max_timing_and_consistent_plan():
         p.join(timeout=60)
     assert [o[0] for o in out] == [0, 1]
     assert all(o[1] == 2 and o[2] == 2.5 and o[3] == 1 for o in out)
+
+
+# ---------------------------------------------------------------------------
+# sharded execution: plan, footprints, dual merge (host logic of mp_shard)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,b,world", [(60, 8, 2), (100, 40, 4), (200, 16, 8), (333, 12, 3)])
+def test_native_plan_matches_python_plan(n, b, world):
+    owner = distributed.native_shard_plan(n, b, world)
+    py = [g for asg in distributed.shard_rounds(n, b, world) for _, g in asg]
+    assert owner.tolist() == py
+
+
+@pytest.mark.parametrize("n,b", [(17, 3), (30, 8), (41, 5), (25, 40)])
+def test_footprints_cover_touched_pairs_and_are_disjoint(n, b):
+    for rnd in schedule.tiled_rounds(n, b):
+        seen = set()
+        for t in rnd.units:
+            fp = distributed.tile_footprint(t, n)
+            touched = set()
+            for (i, j, k) in schedule.tile_triplets(t, n):
+                touched.update(((i, j), (i, k), (j, k)))
+            assert touched <= fp
+            assert not (fp & seen)  # one round's footprints never overlap
+            seen |= fp
+
+
+def test_merge_duals_restores_visit_order():
+    import numpy as np
+    keys = np.arange(10, dtype=np.int64) * 7
+    order = np.array([0, 0, 1, 1, 1, 4, 4, 5, 9, 9], dtype=np.int64)
+    vals = keys * 0.5
+    a = [(keys[m], vals[m], order[m]) for m in (order % 2 == 0, order % 2 == 1)]
+    k, v = distributed.merge_duals(a)
+    assert k.tolist() == keys.tolist() and v.tolist() == vals.tolist()
+
+
+def _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pair_duals, exchange):
+    """One pass of rank `rank` of a sharded solve in the reference's arithmetic
+    (oracle.py_pass restated per tile): own tiles only, footprint exchange
+    after every round, pair rows locally (x identical on every rank)."""
+    from oracle import oracle as orc
+    eps = inst.epsilon
+    plan = distributed.shard_rounds(n, b, world)
+    rounds = schedule.tiled_rounds(n, b)
+    new, order, tix = {}, {}, 0
+    viol = 0.0
+    for rnd, asg in zip(rounds, plan):
+        mine = []
+        for t, g in asg:
+            if g != rank:
+                continue
+            tile = rnd.units[t]
+            mine.append(tile)
+            for (i, j, k) in orc.tile_order(n, b, tile.x, tile.z):
+                ps = (orc._pos(n, i, j), orc._pos(n, i, k), orc._pos(n, j, k))
+                code = ((i * n + j) * n + k) * 3
+                for kd, (pl, m1, m2) in enumerate(((ps[0], ps[1], ps[2]), (ps[1], ps[0], ps[2]),
+                                                   (ps[2], ps[0], ps[1]))):
+                    y = duals.get(code + kd, 0.0)
+                    d0 = x[pl] - x[m1] - x[m2]
+                    viol = max(viol, d0)
+                    delta = d0 + y * 3.0 / eps
+                    theta = eps * delta / 3.0 if delta > 0.0 else 0.0
+                    coef = (y - theta) / eps
+                    if coef != 0.0:
+                        x[pl] += coef
+                        x[m1] -= coef
+                        x[m2] -= coef
+                    if theta > 1e-15:
+                        new[code + kd] = theta
+                        order[code + kd] = tix + t
+        pub = {p: x[orc._pos(n, *p)] for tile in mine for p in distributed.tile_footprint(tile, n)}
+        for other in exchange(pub):
+            for p, v in other.items():
+                x[orc._pos(n, *p)] = v
+        tix += len(rnd.units)
+    viol = max(exchange(viol))
+    return viol, new, order
+
+
+def _shard_worker(rank, world, port, q):
+    import numpy as np
+    import torch.distributed as dist
+    from paper_1901_10084_b200 import instances
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    n, b = 14, 3
+    inst = instances.random_instance(n, seed=11)
+    x = np.zeros(inst.npairs)
+    f = -inst.w_flat / inst.epsilon
+    duals, pd = {}, np.zeros((inst.npairs, 2))
+    for _ in range(3):
+        viol, duals, order = _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pd, exchange)
+        # pair rows on every rank (identical x), as in oracle.py_pass
+        for p in range(inst.npairs):
+            for row in (0, 1):
+                y = pd[p, row]
+                d = inst.d_flat[p]
+                d0 = (x[p] - f[p] - d) if row == 0 else (d - x[p] - f[p])
+                delta = d0 + y * 2.0 / inst.epsilon
+                theta = inst.epsilon * delta / 2.0 if delta > 0.0 else 0.0
+                coef = (y - theta) / inst.epsilon
+                if coef != 0.0:
+                    x[p] = x[p] + coef if row == 0 else x[p] - coef
+                    f[p] -= coef
+                pd[p, row] = theta if theta > 1e-15 else 0.0
+    parts = exchange((np.array(list(duals.keys()), dtype=np.int64),
+                      np.array(list(duals.values())),
+                      np.array([order[k] for k in duals], dtype=np.int64)))
+    keys, vals = distributed.merge_duals(parts)
+    q.put((rank, x.tobytes(), f.tobytes(), keys.tobytes(), vals.tobytes()))
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_protocol_equals_single_worker_oracle():
+    """Two gloo ranks run the sharded protocol (plan, own tiles, footprint
+    exchange after every round, dual merge); x, f and the merged duals equal
+    the reference-order oracle bit for bit."""
+    import numpy as np
+    from oracle import oracle as orc
+    from paper_1901_10084_b200 import instances
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    n, b = 14, 3
+    inst = instances.random_instance(n, seed=11)
+    x = np.zeros(inst.npairs)
+    f = -inst.w_flat / inst.epsilon
+    ones = np.ones(inst.npairs)
+    duals, pd = {}, np.zeros((inst.npairs, 2))
+    for _ in range(3):
+        _, duals = orc.py_pass(n, inst.epsilon, x, f, inst.d_flat, ones, ones, duals, pd,
+                               kind="tiled", b=b)
+    for r in res:
+        assert np.frombuffer(r[1]).tolist() == x.tolist()
+        assert np.frombuffer(r[2]).tolist() == f.tolist()
+        assert np.frombuffer(r[3], dtype=np.int64).tolist() == list(duals.keys())
+        assert np.frombuffer(r[4]).tolist() == list(duals.values())
