@@ -11,7 +11,8 @@ library's stream) of the K timed passes, max over ranks; L2 is flushed
 (256 MiB write) before every timed pass.  ``e2e`` is the same metric through
 the public ``solve()`` API from host arrays (instance upload, every pass,
 per-pass stats and the final x/f/duals download inside the wall-clock).
-Multi-GPU (torchrun) runs independent replicas, one per GPU (weak scaling).
+Multi-GPU (torchrun) runs independent replicas, one per GPU (weak scaling);
+`--sharded` runs one instance over all ranks instead (strong scaling).
 """
 
 from __future__ import annotations
@@ -192,7 +193,11 @@ def run_gpu(args):
     rows = rows_per_pass(n)
 
     # ---- device-resident timing ------------------------------------------------
-    sess = DeviceSession(inst, "tiled", b, device=local)
+    if args.sharded:  # one instance over all ranks (strong scaling)
+        from paper_1901_10084_b200.distributed import ShardedSession
+        sess = ShardedSession(inst, b, device=local).session
+    else:             # one instance per rank (replicas, weak scaling)
+        sess = DeviceSession(inst, "tiled", b, device=local)
     nnz_hist = [0]
     for _ in range(args.warmup):
         nnz_hist.append(sess.run(1)[0].nnz_metric)
@@ -218,7 +223,8 @@ def run_gpu(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_dev, metric_ms = float(tt[0]), float(tt[1])
     sess.close()
-    value = ws * args.steps * rows / t_dev
+    copies = 1 if args.sharded else ws
+    value = copies * args.steps * rows / t_dev
 
     # ---- roofline of the dominant kernel (tile_round_kernel) ------------------
     tx = schedule.touched_pairs(n, b)
@@ -241,7 +247,22 @@ def run_gpu(args):
     if ws > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    sol = solve(inst, SolverConfig(tile_size=b, fixed_passes=total, device=local))
+    if args.sharded:
+        from paper_1901_10084_b200.distributed import ShardedSession
+        shs = ShardedSession(inst, b, device=local)
+        stats = shs.run(total)
+        xs, fs = shs.state()
+        dk, dv = shs.duals()
+        shs.close()
+
+        class _Sol:  # the fields the JSON line reads
+            pass
+        sol = _Sol()
+        sol.stats = [type("S", (), {"primal_objective": s_.primal_objective,
+                                    "max_violation": s_.max_violation}) for s_ in stats]
+        sol.duals = type("D", (), {"nnz": staticmethod(lambda: len(dk))})
+    else:
+        sol = solve(inst, SolverConfig(tile_size=b, fixed_passes=total, device=local))
     t_e2e = time.perf_counter() - t0
     if ws > 1:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
@@ -250,7 +271,7 @@ def run_gpu(args):
     m = inst.npairs
     h2d = 8 * 4 * m  # d, w, reg_x, reg_f
     d2h = total * 64 + 8 * 2 * m + 16 * m + 16 * sol.duals.nnz()
-    e2e = {"value": ws * total * rows / t_e2e, "unit": UNIT,
+    e2e = {"value": copies * total * rows / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": h2d / total, "d2h_bytes_per_step": d2h / total,
            "wall_s": t_e2e, "passes": total}
 
@@ -268,12 +289,14 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.sharded else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator with the BASELINE config shape)",
             "config": {"workload": workload_name(spec, b), "n": n, "tile_b": b,
                        "passes_in_config": spec.passes,
                        "l2": "flushed (256 MiB write) before every timed pass",
-                       "parallelism": "replicas" if ws > 1 else "1 GPU"},
+                       "parallelism": (f"sharded x{ws} (one instance)" if args.sharded else
+                                       "replicas" if ws > 1 else "1 GPU")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
             "final": {"primal": sol.stats[-1].primal_objective,
@@ -295,6 +318,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="one instance over all ranks (strong scaling) instead of replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
