@@ -116,7 +116,25 @@ struct TileArgs {
     int32_t nwc;  // compute warps per CTA (the rest are ring producers)
     StepConsts kc;
     unsigned long long *trace;  // optional cycle counters (mp_trace), null = off
+    int32_t round_id;           // schedule round of this launch
+    int32_t lw;                 // active lanes per warp slot row (<= 32)
+    int32_t tl_round;           // MP_TIMELINE builds: round whose first tile is traced
 };
+
+#ifdef MP_TIMELINE
+// Diagnostic timeline (tools/timeline.py): per (band, warp, batch) the clock64
+// values [wait start, work start, work end, cold flag, levels replayed, lookup,
+// math, append cycles]; warp slot 15 of each band holds [clock64,
+// globaltimer] at the sweep start and end.
+constexpr int TL_MAXB = 512;
+constexpr int TL_REC = 8;  // u64 per batch record
+constexpr int TL_SLOTS = 8 * 16 * TL_MAXB * TL_REC;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 // trace slots (cycles summed over warps / CTAs; see tools/trace_pass.py)
 enum TraceSlot {
@@ -150,6 +168,14 @@ struct CtaConst {
     unsigned long long *trace;
     StepConsts kc;
     int32_t b, nt, xsize, dbg;
+    int32_t C, band, RB;  // cluster size, this CTA's row band, rows per band
+    int32_t nwc;          // compute warps per CTA
+    int32_t tl;           // MP_TIMELINE: this CTA records its timeline
+    int32_t B32;          // shared address of the aligned staging base
+    int32_t lw;           // active lanes per warp slot row
+    uint32_t rep_lo;      // shared address of WK (replicated in every band)
+    uint32_t zero_lo;     // ... of the zero row (end of WK)
+    uint32_t rk_lo;       // ... of RK
 };
 
 // ---------------------------------------------------------------------------
@@ -160,49 +186,110 @@ struct CtaConst {
 // move, nothing stored) -- the same values the reference computes.
 // Correctly rounded a/b from rb = RN(1/b) (Markstein): q0 = RN(a*rb) is
 // within one ulp of a/b, the residual a - q0*b is exact with an FMA, and one
-// correction RN(q0 + r*rb) rounds correctly.  Outside the safe exponent range
-// (or for 0, inf, nan) it falls back to IEEE division; the host only enables
-// it for divisors whose significand is not all ones.  Verified bit for bit
-// against __ddiv_rn by mp_check_division (tests/test_gpu_parity.py).
+// correction RN(q0 + r*rb) rounds correctly.  The host enables it only for
+// divisors with 2^-60 <= |b| <= 2^60 whose significand is not all ones; then
+// a dividend with 2^-900 <= |a| <= 2^900 keeps every intermediate normal, and
+// anything else (0, subnormal, huge, inf, nan) takes IEEE division.  The range
+// test reads only a, so it runs beside the multiply chain.  Verified bit for
+// bit against __ddiv_rn by mp_check_division (tests/test_gpu_parity.py).
+// IEEE division, out of line: one copy for every rarely taken slow path
+// (keeps the exact step's code small enough to stay in the instruction cache)
+__device__ __noinline__ double ddiv_ieee(double a, double b) { return __ddiv_rn(a, b); }
+
 __device__ __forceinline__ double div_rn(double a, double b, double rb) {
+    const double aa = fabs(a);
     const double q0 = __dmul_rn(a, rb);
     const double r = __fma_rn(-q0, b, a);
     const double q1 = __fma_rn(r, rb, q0);
-    const double aq = fabs(q1);
-    if (!(aq > 0x1p-960 && aq < 0x1p+960)) return __ddiv_rn(a, b);
+    if (!(aa >= 0x1p-900 && aa <= 0x1p+900)) return ddiv_ieee(a, b);
     return q1;
 }
 
-
 __device__ __forceinline__ double div_eps(double a, const StepConsts &k) {
-    return k.reps != 0.0 ? div_rn(a, k.eps, k.reps) : __ddiv_rn(a, k.eps);
+    return k.reps != 0.0 ? div_rn(a, k.eps, k.reps) : ddiv_ieee(a, k.eps);
 }
 
+// s = (w_plus + w_m1) + w_m2 of a row (_kernels.py:118); 3 exactly for W = I
+template <bool UNIT>
+__device__ __forceinline__ double row_s(double wp, double wm1, double wm2) {
+    return UNIT ? 3.0 : __dadd_rn(__dadd_rn(wp, wm1), wm2);
+}
+
+// One metric row given its value d0 = (plus - m1) - m2 and yq = (y*s)/eps
+// (any value when y = 0): the reference step (_kernels.py:115-125).  Returns
+// whether x moved (coef != 0); theta goes to th.
+template <bool UNIT>
+__device__ __forceinline__ bool row_step(double &p, double &m1, double &m2, double wp, double wm1,
+                                         double wm2, double y, double yq, double d0,
+                                         const StepConsts &k, double &viol, double &th) {
+    viol = d0 > viol ? d0 : viol;
+    th = 0.0;
+    if (y == 0.0 && !(d0 > 0.0)) return false;
+    const double delta = y == 0.0 ? d0 : __dadd_rn(d0, yq);
+    double theta = 0.0;
+    if (delta > 0.0)
+        theta = UNIT ? div_rn(__dmul_rn(k.eps, delta), 3.0, k.r3)
+                     : ddiv_ieee(__dmul_rn(k.eps, delta), row_s<UNIT>(wp, wm1, wm2));
+    th = theta;
+    const double coef = div_eps(__dsub_rn(y, theta), k);
+    if (coef == 0.0) return false;
+    if (UNIT) {
+        p = __dadd_rn(p, coef);
+        m1 = __dsub_rn(m1, coef);
+        m2 = __dsub_rn(m2, coef);
+    } else {
+        p = __dadd_rn(p, __dmul_rn(coef, wp));
+        m1 = __dsub_rn(m1, __dmul_rn(coef, wm1));
+        m2 = __dsub_rn(m2, __dmul_rn(coef, wm2));
+    }
+    return true;
+}
+
+// yq = (y*s)/eps of the three rows (kinds IJ, IK, JK), from the duals alone
+template <bool UNIT>
+__device__ __forceinline__ void rows_yq(const double (&y)[3], double wa, double wc, double we,
+                                        const StepConsts &k, double (&yq)[3]) {
+    const double s0 = row_s<UNIT>(wa, wc, we), s1 = row_s<UNIT>(wc, wa, we), s2 = row_s<UNIT>(we, wa, wc);
+    yq[0] = y[0] != 0.0 ? div_eps(__dmul_rn(y[0], s0), k) : 0.0;
+    yq[1] = y[1] != 0.0 ? div_eps(__dmul_rn(y[1], s1), k) : 0.0;
+    yq[2] = y[2] != 0.0 ? div_eps(__dmul_rn(y[2], s2), k) : 0.0;
+}
+
+// The three rows of triplet (i,j,k) in kind order IJ, IK, JK (_kernels.py:97-
+// 109), p = x_ij, c = x_ik, e = x_jk.  The row values are formed up front and
+// re-formed only after a row moved x, so each row sees exactly the value the
+// reference computes at its turn.  Returns whether x moved.
+template <bool UNIT>
+__device__ __forceinline__ bool step3(double &p, double &c, double &e, double wa, double wc,
+                                      double we, const double (&y)[3], const double (&yq)[3],
+                                      const StepConsts &k, double &viol, double (&th)[3]) {
+    double d0 = __dsub_rn(__dsub_rn(p, c), e);
+    double d1 = __dsub_rn(__dsub_rn(c, p), e);
+    double d2 = __dsub_rn(__dsub_rn(e, p), c);
+    bool moved = false;
+    if (row_step<UNIT>(p, c, e, wa, wc, we, y[0], yq[0], d0, k, viol, th[0])) {  // x_ij <= x_ik + x_jk
+        moved = true;
+        d1 = __dsub_rn(__dsub_rn(c, p), e);
+        d2 = __dsub_rn(__dsub_rn(e, p), c);
+    }
+    if (row_step<UNIT>(c, p, e, wc, wa, we, y[1], yq[1], d1, k, viol, th[1])) {  // x_ik <= x_ij + x_jk
+        moved = true;
+        d2 = __dsub_rn(__dsub_rn(e, p), c);
+    }
+    if (row_step<UNIT>(e, p, c, we, wa, wc, y[2], yq[2], d2, k, viol, th[2])) moved = true;  // x_jk
+    return moved;
+}
+
+// One row with everything formed in place (serial kernel).
 template <bool UNIT>
 __device__ __forceinline__ double dykstra_row(double &p, double &m1, double &m2, double wp,
                                               double wm1, double wm2, double y,
                                               const StepConsts &k, double &viol) {
     const double d0 = __dsub_rn(__dsub_rn(p, m1), m2);
-    viol = d0 > viol ? d0 : viol;
-    if (y == 0.0 && !(d0 > 0.0)) return 0.0;
-    const double s = UNIT ? 3.0 : __dadd_rn(__dadd_rn(wp, wm1), wm2);
-    const double delta = y == 0.0 ? d0 : __dadd_rn(d0, div_eps(__dmul_rn(y, s), k));
-    double theta = 0.0;
-    if (delta > 0.0)
-        theta = UNIT ? div_rn(__dmul_rn(k.eps, delta), 3.0, k.r3) : __ddiv_rn(__dmul_rn(k.eps, delta), s);
-    const double coef = div_eps(__dsub_rn(y, theta), k);
-    if (coef != 0.0) {
-        if (UNIT) {
-            p = __dadd_rn(p, coef);
-            m1 = __dsub_rn(m1, coef);
-            m2 = __dsub_rn(m2, coef);
-        } else {
-            p = __dadd_rn(p, __dmul_rn(coef, wp));
-            m1 = __dsub_rn(m1, __dmul_rn(coef, wm1));
-            m2 = __dsub_rn(m2, __dmul_rn(coef, wm2));
-        }
-    }
-    return theta;
+    const double yq = y != 0.0 ? div_eps(__dmul_rn(y, row_s<UNIT>(wp, wm1, wm2)), k) : 0.0;
+    double th;
+    row_step<UNIT>(p, m1, m2, wp, wm1, wm2, y, yq, d0, k, viol, th);
+    return th;
 }
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *addr, double v) {
@@ -225,6 +312,39 @@ __device__ __forceinline__ double warp_max(double v) {
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
+// ---- thread-block cluster primitives (one tile over C SMs) -------------------
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// shared::cta address -> the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t a, unsigned rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_cluster(uint32_t a, int v) {
+    asm volatile("st.release.cluster.shared::cluster.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cluster(uint32_t a) {
+    int v;
+    asm volatile("ld.acquire.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // 32-bit shared-window addresses: the per-slot constants already hold the
 // absolute address, so the hot loop issues LDS [R] with no base add
 __device__ __forceinline__ double ld_sh(uint32_t a) {
@@ -317,11 +437,12 @@ __device__ __forceinline__ void rd_init(WarpDuals *w, const DualPool &p, int64_t
     __syncwarp();
 }
 
-// Consume every entry with key in [base, base+96); lane l receives the values
-// of its kinds 0..2.  Warp-collective.
+// Consume every entry with key in [base, base + S*96) (one level of this
+// warp's S slots); lane l receives y[s][kind] of its slots.  Warp-collective.
+template <int S>
 __device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint32_t base, int lane,
-                                          double &y0, double &y1, double &y2) {
-    const uint32_t lim = base + 96u;
+                                          double (&y)[S][3]) {
+    const uint32_t lim = base + (uint32_t)(S * 96);
     uint32_t head = w->head;
     int pos = w->pos, cur = w->cur;
     while (head < lim) {
@@ -332,12 +453,15 @@ __device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint3
             const int src = __ffs(mm) - 1;
             mm &= mm - 1;
             const uint32_t off = w->buf[cur].keys[src] - base;
-            if (off / 3u == (uint32_t)lane) {
+            const uint32_t sl = off / 96u, r = off - 96u * sl;
+            if (r / 3u == (uint32_t)lane) {
                 const double v = w->buf[cur].vals[src];
-                const uint32_t kd = off - 3u * (uint32_t)lane;
-                if (kd == 0) y0 = v;
-                else if (kd == 1) y1 = v;
-                else y2 = v;
+                const uint32_t kd = r - 3u * (uint32_t)lane;
+#pragma unroll
+                for (int ss = 0; ss < S; ++ss)
+#pragma unroll
+                    for (int kk = 0; kk < 3; ++kk)
+                        if (sl == (uint32_t)ss && kd == (uint32_t)kk) y[ss][kk] = v;
             }
         }
         pos += __popc(m);
@@ -448,15 +572,19 @@ __device__ __forceinline__ void wr_finish(WarpDuals *w, const DualPool &p, PassC
 // WR / WK rings for array `g` (x or winvx) into ring arrays `wr`, `wk`.
 // Predicates select exactly the pairs this tile touches that live in the
 // rings (see the layout note above); nothing else is read or written.
+// A cluster CTA stages only the WR rows of its band, [r0, r1) relative to
+// ilo (stored from row 0 of its WR), and every CTA stages the whole WK; with
+// with_wk = false the WK part is skipped (write-back by the last band only).
 template <int W, bool LOAD>
 __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld, double *g,
-                                           double *wr, double *wk, int blk, int tid, int nt) {
+                                           double *wr, double *wk, int blk, int tid, int nt,
+                                           int r0, int r1, bool with_wk) {
     const int j0 = blk * BLK;
-    // WR: rows i in R x 16 columns j (row-contiguous in global memory)
-    const int nwr = b * BLK;
+    // WR: rows i in the band x 16 columns j (row-contiguous in global memory)
+    const int nwr = (r1 - r0) * BLK;
     for (int e = tid; e < nwr; e += nt) {
         const int ii = e / BLK, jj = e - ii * BLK;
-        const int i = T.ilo + ii, j = j0 + jj;
+        const int i = T.ilo + r0 + ii, j = j0 + jj;
         if (i <= T.ihi && j >= T.jlo && j <= T.jhi && j < T.klo && i < j) {
             double *s = wr + ii * W + (j & (W - 1));
             double *gp = g + (int64_t)i * ld + j;
@@ -464,6 +592,7 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld,
             else *gp = *s;
         }
     }
+    if (!with_wk) return;
     // WK: 16 rows j x columns k in K; a warp covers 4 consecutive k (one
     // 32-byte sector per row) x 8 rows j
     const int kq = (b + 3) / 4;
@@ -482,11 +611,11 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld,
     }
 }
 
-// RK block: rows i in R, columns k in K, i < k.
+// RK block: rows i in R (relative rows [r0, r1)), columns k in K, i < k.
 template <bool LOAD>
 __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, double *g,
-                                         double *rk, int tid, int nt) {
-    for (int e = tid; e < b * b; e += nt) {
+                                         double *rk, int tid, int nt, int r0, int r1) {
+    for (int e = r0 * b + tid; e < r1 * b; e += nt) {
         const int ii = e / b, kk = e - ii * b;
         const int i = T.ilo + ii, k = T.klo + kk;
         if (i <= T.ihi && k <= T.z && i < k) {
@@ -495,60 +624,6 @@ __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, d
             else *gp = rk[e];
         }
     }
-}
-
-// ---------------------------------------------------------------------------
-// cold path: a warp replays one slot of one level with the full step
-// ---------------------------------------------------------------------------
-// pa/pc/pe are the shared addresses of x_ij, x_ik, x_jk the hot path computed
-// (the zero row for inactive slots, where every row value is 0 and no dual
-// exists, so the exact step is a no-op there).
-template <int W, bool UNIT>
-__device__ __noinline__ double cold_slot(unsigned char *sm, const CtaConst *cc, WarpDuals *wd,
-                                         uint32_t base, int pa, int pc, int pe, double viol) {
-    const int tid = threadIdx.x, lane = tid & 31;
-#ifdef MP_TRACE
-    long long q0 = clock64();
-#endif
-    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    if (wd->head < base + 96u) rd_lookup(wd, cc->rp, base, lane, y0, y1, y2);
-#ifdef MP_TRACE
-    long long q1 = clock64();
-#endif
-    double p = ld_sh(pa), c = ld_sh(pc), e = ld_sh(pe);
-    const double d0 = __dsub_rn(__dsub_rn(p, c), e);
-    const double d1 = __dsub_rn(__dsub_rn(c, p), e);
-    const double d2 = __dsub_rn(__dsub_rn(e, p), c);
-    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    if ((d0 > 0.0) | (d1 > 0.0) | (d2 > 0.0) | (y0 != 0.0) | (y1 != 0.0) | (y2 != 0.0)) {
-        double wa = 1.0, wc = 1.0, we = 1.0;
-        if (!UNIT) {
-            const int xb = cc->xsize * 8;  // winv staging mirrors the x layout
-            wa = ld_sh(pa + xb);
-            wc = ld_sh(pc + xb);
-            we = ld_sh(pe + xb);
-        }
-        const StepConsts k = cc->kc;
-        t0 = dykstra_row<UNIT>(p, c, e, wa, wc, we, y0, k, viol);  // IJ: x_ij <= x_ik + x_jk
-        t1 = dykstra_row<UNIT>(c, p, e, wc, wa, we, y1, k, viol);  // IK: x_ik <= x_ij + x_jk
-        t2 = dykstra_row<UNIT>(e, p, c, we, wa, wc, y2, k, viol);  // JK: x_jk <= x_ij + x_ik
-        st_sh(pa, p);
-        st_sh(pc, c);
-        st_sh(pe, e);
-    }
-#ifdef MP_TRACE
-    long long q2 = clock64();
-#endif
-    wr_append(wd, cc->wp, cc->ctr, cc->T.stream0 + (tid >> 5), base, lane, t0, t1, t2);
-#ifdef MP_TRACE
-    if (cc->trace && lane == 0) {
-        long long q3 = clock64();
-        atomicAdd(&cc->trace[TR_C_LOOKUP], (unsigned long long)(q1 - q0));
-        atomicAdd(&cc->trace[TR_C_MATH], (unsigned long long)(q2 - q1));
-        atomicAdd(&cc->trace[TR_C_APPEND], (unsigned long long)(q3 - q2));
-    }
-#endif
-    return viol;
 }
 
 // ---------------------------------------------------------------------------
@@ -565,10 +640,11 @@ __device__ __noinline__ double cold_slot(unsigned char *sm, const CtaConst *cc, 
 template <int W>
 struct SmemMap {
     int b;
+    int rb;  // WR rows staged by this CTA (its band; b without a cluster)
     __device__ __host__ int wr() const { return 0; }
-    __device__ __host__ int wk() const { return b * W * 8; }
-    __device__ __host__ int zero() const { return 2 * b * W * 8; }
-    __device__ __host__ int rk() const { return 2 * b * W * 8 + W * 8; }
+    __device__ __host__ int wk() const { return rb * W * 8; }
+    __device__ __host__ int zero() const { return (rb + b) * W * 8; }
+    __device__ __host__ int rk() const { return (rb + b) * W * 8 + W * 8; }
     __device__ __host__ int xbytes() const { return rk() + ((b * b * 8 + W * 8 - 1) / (W * 8)) * W * 8; }
 };
 
@@ -616,10 +692,11 @@ __device__ __forceinline__ unsigned triplet_violated(double a, double c, double 
 // Branch-free: inactive slots read the zero row (all row values 0).  With
 // t = fl(a - c), u = fl(e - a):  (d0 > 0 || d1 > 0) <=> |t| > e  and
 // d2 > 0 <=> u > c, exactly (see triplet_violated).
+// Shared addresses of x_ij, x_ik, x_jk of this thread's S slots at level L
+// (the zero row for a slot with no triplet at L).
 template <int S, int W, bool ALIAS>
-__device__ __forceinline__ bool level_hot(const unsigned char *sm, const SlotGeom<S> &G, int L,
-                                          int b, int ihi, int klo, int (&pa)[S], int (&pc)[S],
-                                          int (&pe)[S], const double (&xcr)[S]) {
+__device__ __forceinline__ void slot_addrs(const SlotGeom<S> &G, int L, int b, int ihi, int klo,
+                                           int (&pa)[S], int (&pc)[S], int (&pe)[S]) {
     const int L8 = L * 8;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -635,10 +712,21 @@ __device__ __forceinline__ bool level_hot(const unsigned char *sm, const SlotGeo
             pc[s] = act ? G.pik[s] : G.zero;
         } else {
             pa[s] = jm | G.wr[s];
+#ifndef MP_EXP_BCAST
             pe[s] = jm | G.wk[s];
+#else
+            pe[s] = G.zero;  // timing experiment: x_jk loads become broadcasts
+#endif
             pc[s] = G.pik[s];
         }
     }
+}
+
+template <int S, int W, bool ALIAS>
+__device__ __forceinline__ bool level_hot(const unsigned char *sm, const SlotGeom<S> &G, int L,
+                                          int b, int ihi, int klo, int (&pa)[S], int (&pc)[S],
+                                          int (&pe)[S], const double (&xcr)[S]) {
+    slot_addrs<S, W, ALIAS>(G, L, b, ihi, klo, pa, pc, pe);
     double xa[S], xc[S], xe[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -655,6 +743,214 @@ __device__ __forceinline__ bool level_hot(const unsigned char *sm, const SlotGeo
         bad = bad | (fabs(t) > xe[s]) | (u > xc[s]);
     }
     return bad;
+}
+
+// Slot geometry of this thread: q = (warp*S + s)*lw + lane within the band
+// [r0, r1) of the tile, (i, k) = (ilo + r0 + q/b, klo + q%b); a warp may use
+// only lw < 32 lanes per slot row (less exact-step work per warp).
+template <int S, int W>
+__device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, const SmemMap<W> &M,
+                                          int B32, int b, int r0, int r1, int warp, int lane, int lw) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int q = (warp * S + s) * lw + lane;  // lanes >= lw idle (fewer slots per warp)
+        const int ii = r0 + q / b, kk = q - (q / b) * b;
+        const int i = T.ilo + ii, k = T.klo + kk;
+        const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
+        const bool ok = lane < lw && q < (r1 - r0) * b && i <= T.ihi && k <= T.z && js <= je;
+        G.ik8[s] = ok ? 8 * (i + k) : 0;
+        G.off[s] = ok ? i + k + js : 0x3fffffff;
+        G.span[s] = ok ? (unsigned)(je - js) : 0u;
+        G.pik[s] = B32 + (ok ? M.rk() + 8 * (ii * b + kk) : M.zero());
+        G.wr[s] = B32 + (ok ? M.wr() + (ii - r0) * W * 8 : M.zero());
+        G.wk[s] = B32 + (ok ? M.wk() + kk * W * 8 : M.zero());
+        G.rkr[s] = B32 + (ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero());
+        G.rkc[s] = B32 + (ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero());
+    }
+    G.zero = B32 + M.zero();
+}
+
+// ---------------------------------------------------------------------------
+// cold path: the exact reference step for the levels of a batch that need it
+// ---------------------------------------------------------------------------
+// Levels [first, Le] of the batch starting at L0, in order.  A level is
+// replayed if the hot check flagged it (bit Lc-L0 of `flagged`), if it holds
+// one of this warp's stored duals, or if an earlier level of this batch moved
+// x (the hot check read values this warp has since changed; other warps'
+// values were final before the batch started).  Per level: the duals of all S
+// slots in one pass over the warp stream, the three rows of every slot that
+// needs them (reference association, _kernels.py:115-125), and the new duals
+// appended in key order.  Out of line: the hot loop keeps its registers.
+// Exact step of one slot of one level for the whole warp (used with S > 1,
+// where cold_batch's live state would not fit the registers).  pa/pc/pe are
+// the slot's shared addresses (the zero row for inactive lanes).  Returns the
+// updated violation; `fwd` is set if a value was forwarded to a later band.
+template <int W, bool UNIT>
+__device__ __noinline__ double cold_slot(const CtaConst *cc, WarpDuals *wd, int warp, uint32_t base,
+                                         int pa, int pc, int pe, double viol, bool &fwd) {
+    const int lane = threadIdx.x & 31;
+    double y[1][3] = {{0.0, 0.0, 0.0}};
+    if (wd->head < base + 96u) rd_lookup<1>(wd, cc->rp, base, lane, y);
+    double p = ld_sh(pa), c = ld_sh(pc), e = ld_sh(pe);
+    double th[3] = {0.0, 0.0, 0.0};
+    const bool need = (fabs(__dsub_rn(p, c)) > e) | (__dsub_rn(e, p) > c) | (y[0][0] != 0.0) |
+                      (y[0][1] != 0.0) | (y[0][2] != 0.0);
+    if (need) {
+        double wa = 1.0, wc = 1.0, we = 1.0;
+        if (!UNIT) {
+            const int xb = cc->xsize * 8;
+            wa = ld_sh(pa + xb);
+            wc = ld_sh(pc + xb);
+            we = ld_sh(pe + xb);
+        }
+        double yq[3];
+        rows_yq<UNIT>(y[0], wa, wc, we, cc->kc, yq);
+        step3<UNIT>(p, c, e, wa, wc, we, y[0], yq, cc->kc, viol, th);
+        st_sh(pa, p);
+        st_sh(pc, c);
+        st_sh(pe, e);
+        const int C = cc->C, band = cc->band;
+        if (C > 1 && band + 1 < C) {  // forwarding rule: see cold_batch
+            const uint32_t ue = (uint32_t)pe;
+            int dlast = band;
+            if (ue >= cc->rep_lo && ue < cc->zero_lo) dlast = C - 1;
+            else if (ue >= cc->rk_lo) dlast = min(C - 1, (int)((ue - cc->rk_lo) / (8u * (uint32_t)cc->b)) / cc->RB);
+            for (int d = band + 1; d <= dlast; ++d) st_cluster_f64(mapa(ue, d), e);
+            fwd |= dlast > band;
+        }
+    }
+    const int64_t stream = cc->T.stream0 + (int64_t)cc->band * cc->nwc + warp;
+    if (__any_sync(0xffffffffu, (th[0] > THETA_FLOOR) | (th[1] > THETA_FLOOR) | (th[2] > THETA_FLOOR)))
+        wr_append(wd, cc->wp, cc->ctr, stream, base, lane, th[0], th[1], th[2]);
+    return viol;
+}
+
+// One level replayed exactly (S > 1): per slot, if some lane of the warp has
+// a violated row or the slot holds a stored dual, the out-of-line cold_slot.
+template <int S, int W, bool UNIT, bool ALIAS>
+__device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned char *sm,
+                                           const SlotGeom<S> &G, const CtaConst *cc, WarpDuals *wd,
+                                           int warp, int b, int ihi, int klo, double (&xcr)[S],
+                                           uint32_t &head, double &viol, bool &fwd) {
+    int pa[S], pc[S], pe[S];
+    level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
+    bool moved = false;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const uint32_t bs = base0 + (uint32_t)(s * 96);
+        const double a = ld_sh(pa[s]), c = ld_sh(pc[s]), e = ld_sh(pe[s]);
+        const bool bad = (fabs(__dsub_rn(a, c)) > e) | (__dsub_rn(e, a) > c);
+        if (__any_sync(0xffffffffu, bad) || head < bs + 96u) {
+            viol = cold_slot<W, UNIT>(cc, wd, warp, bs, pa[s], pc[s], pe[s], viol, fwd);
+            head = wd->head;
+            if (!ALIAS) xcr[s] = ld_sh(pc[s]);  // the exact step may move x_ik
+            moved = true;
+        }
+    }
+    return moved;
+}
+
+#ifndef MP_COLD_INLINE
+#define MP_COLD_INLINE __noinline__
+#endif
+template <int S, int W, bool UNIT, bool ALIAS>
+__device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned flagged,
+                                          const CtaConst *cc, WarpDuals *wd, int warp, double viol) {
+    const int lane = threadIdx.x & 31;
+    const TileDesc &T = cc->T;
+    const int b = cc->b, C = cc->C, band = cc->band;
+    const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
+    const SmemMap<W> M{b, cc->RB};
+    SlotGeom<S> G;
+    slot_geom<S, W>(G, T, M, cc->B32, b, r0, r1, warp, lane, cc->lw);
+    constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
+    const int64_t stream = T.stream0 + (int64_t)band * cc->nwc + warp;
+    const StepConsts k = cc->kc;
+    const int xb = cc->xsize * 8;  // winv staging mirrors the x layout (general W)
+    const bool fwd_band = C > 1 && band + 1 < C;
+    bool dirty = false, fwd = false;
+#ifdef MP_TIMELINE
+    long long tq0 = clock64(), c_lk = 0, c_mt = 0, c_ap = 0, nlev = 0;
+#endif
+    for (int Lc = first; Lc <= Le; ++Lc) {
+        const uint32_t base = (uint32_t)(Lc - T.Lbeg) * PER_LEVEL;
+        const bool has_dual = wd->head < base + PER_LEVEL;
+        if (!dirty && !has_dual && !((flagged >> (Lc - L0)) & 1u)) continue;
+#ifdef MP_TIMELINE
+        ++nlev;
+        long long tq = clock64();
+#endif
+        int pa[S], pc[S], pe[S];
+        slot_addrs<S, W, ALIAS>(G, Lc, b, T.ihi, T.klo, pa, pc, pe);
+        bool moved = false;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {  // slot by slot: keys are ordered by slot
+            const uint32_t bs = base + (uint32_t)(s * 96);
+            double y[1][3] = {{0.0, 0.0, 0.0}};
+            if (wd->head < bs + 96u) rd_lookup<1>(wd, cc->rp, bs, lane, y);
+#ifdef MP_TIMELINE
+            { const long long t = clock64(); c_lk += t - tq; tq = t; }
+#endif
+            double th[3] = {0.0, 0.0, 0.0};
+            double p = ld_sh(pa[s]), c = ld_sh(pc[s]), e = ld_sh(pe[s]);
+            double wa = 1.0, wc = 1.0, we = 1.0;
+            if (!UNIT) {
+                wa = ld_sh(pa[s] + xb);
+                wc = ld_sh(pc[s] + xb);
+                we = ld_sh(pe[s] + xb);
+            }
+            const bool need = (fabs(__dsub_rn(p, c)) > e) | (__dsub_rn(e, p) > c) |
+                              (y[0][0] != 0.0) | (y[0][1] != 0.0) | (y[0][2] != 0.0);
+            bool any_th = false;
+            if (need) {
+                double yq[3];
+                rows_yq<UNIT>(y[0], wa, wc, we, k, yq);
+                step3<UNIT>(p, c, e, wa, wc, we, y[0], yq, k, viol, th);
+                st_sh(pa[s], p);
+                st_sh(pc[s], c);
+                st_sh(pe[s], e);
+                moved = true;
+                any_th = (th[0] > THETA_FLOOR) | (th[1] > THETA_FLOOR) | (th[2] > THETA_FLOOR);
+                // Cluster: x_ij and x_ik lie in this band's own rows (WR, or RK
+                // rows i) and no later band (larger rows) reads those; x_jk is
+                // read later by every later band if it is in WK (j > ihi), and
+                // by the later bands up to the owner of row j if it is RK row j.
+                if (fwd_band) {
+                    const uint32_t ue = (uint32_t)pe[s];
+                    int dlast = band;
+                    if (ue >= cc->rep_lo && ue < cc->zero_lo) dlast = C - 1;
+                    else if (ue >= cc->rk_lo)
+                        dlast = min(C - 1, (int)((ue - cc->rk_lo) / (8u * (uint32_t)b)) / cc->RB);
+                    for (int d = band + 1; d <= dlast; ++d) st_cluster_f64(mapa(ue, d), e);
+                    fwd |= dlast > band;
+                }
+            }
+#ifdef MP_TIMELINE
+            { const long long t = clock64(); c_mt += t - tq; tq = t; }
+#endif
+            if (__any_sync(0xffffffffu, any_th))
+                wr_append(wd, cc->wp, cc->ctr, stream, bs, lane, th[0], th[1], th[2]);
+#ifdef MP_TIMELINE
+            { const long long t = clock64(); c_ap += t - tq; tq = t; }
+#endif
+        }
+        dirty |= __any_sync(0xffffffffu, moved);
+    }
+#ifdef MP_TIMELINE
+    if (cc->tl && lane == 0) {  // the caller's batch record, slots 4..7
+        const int nb = wd->pad;  // batch index parked by the caller
+        if (nb < TL_MAXB) {
+            unsigned long long *r = cc->trace + (((size_t)band * 16 + warp) * TL_MAXB + nb) * TL_REC;
+            r[4] = (unsigned long long)nlev;
+            r[5] = (unsigned long long)c_lk;
+            r[6] = (unsigned long long)c_mt;
+            r[7] = (unsigned long long)(clock64() - tq0 - c_lk - c_mt);
+        }
+    }
+#endif
+    // forwarded values land in the later bands before this warp's progress does
+    if (__any_sync(0xffffffffu, fwd)) fence_cluster();
+    return viol;
 }
 
 // ---------------------------------------------------------------------------
@@ -694,25 +990,46 @@ __device__ __forceinline__ void wait_geq(const int *p, int v, bool sleep) {
 }
 
 struct TileSync {
-    int done[32];    // last level each compute warp finished
-    int landed;      // highest ring block landed
-    int lo_res;      // producer's lowest resident block (for the epilogue)
-    int hi_issued;   // producer's highest issued block (for the epilogue)
-    int pslow, pfast;  // producer-internal broadcast
+    int done[32];       // last level each compute warp finished
+    int landed_by[16];  // highest ring block landed, per CTA of the cluster
+    int lo_res;         // producer's lowest resident block (for the epilogue)
+    int hi_issued;      // producer's highest issued block (for the epilogue)
+    int pslow, pfast;   // producer-internal broadcast
 };
 
-// Re-derive on the cold path whether slot s has a violated row.
-__device__ __forceinline__ bool slot_violated(const unsigned char *sm, int pa, int pc, int pe) {
-    const double a = ld_sh(pa), c = ld_sh(pc), e = ld_sh(pe);
-    return (fabs(__dsub_rn(a, c)) > e) | (__dsub_rn(e, a) > c);
+// Lowest ring block landed in every CTA of the cluster: a block may be used
+// (and an upstream band may forward writes into it) only once every band's
+// copy of it has landed.
+__device__ __forceinline__ int landed_min(TileSync &ts, int C) {
+    int m = ld_acquire_cluster(smem_u32(&ts.landed_by[0]));
+    for (int d = 1; d < C; ++d) m = min(m, ld_acquire_cluster(smem_u32(&ts.landed_by[d])));
+    return m;
+}
+
+// Back-off of the progress spins: a sleeping warp frees issue slots but
+// wakes late (measured: no difference between 0, 5, 20 and 100 ns).
+#ifndef MP_SPIN_NS
+#define MP_SPIN_NS 20
+#endif
+__device__ __forceinline__ void spin_pause() {
+    if (MP_SPIN_NS > 0) __nanosleep(MP_SPIN_NS);
 }
 
 // spin until *p >= v (acquire); returns the value seen
 __device__ __forceinline__ int wait_geq_v(const int *p, int v) {
     int x = ld_acquire(p);
     while (x < v) {
-        __nanosleep(20);
+        spin_pause();
         x = ld_acquire(p);
+    }
+    return x;
+}
+// the same for a flag in another CTA of the cluster (shared::cluster address)
+__device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
+    int x = ld_acquire_cluster(a);
+    while (x < v) {
+        spin_pause();
+        x = ld_acquire_cluster(a);
     }
     return x;
 }
@@ -720,31 +1037,6 @@ __device__ __forceinline__ int wait_geq_v(const int *p, int v) {
 #ifndef MP_BATCH
 #define MP_BATCH 4
 #endif
-
-// One level done exactly the old way: hot check, then the exact step for the
-// slots that need it.  Returns whether the cold path ran.
-template <int S, int W, bool UNIT, bool ALIAS>
-__device__ __forceinline__ bool level_full(int L, uint32_t base0, unsigned char *sm,
-                                           const SlotGeom<S> &G, CtaConst &cc, WarpDuals *wd,
-                                           int b, int ihi, int klo, double (&xcr)[S],
-                                           uint32_t &head, double &viol) {
-    int pa[S], pc[S], pe[S];
-    const bool bad = level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
-    const bool go_cold = __any_sync(0xffffffffu, bad) || head < base0 + (uint32_t)(S * 96);
-    if (go_cold) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const uint32_t bs = base0 + (uint32_t)(s * 96);
-            if (__any_sync(0xffffffffu, bad && slot_violated(sm, pa[s], pc[s], pe[s])) ||
-                head < bs + 96u) {
-                viol = cold_slot<W, UNIT>(sm, &cc, wd, bs, pa[s], pc[s], pe[s], viol);
-                head = wd->head;
-                if (!ALIAS) xcr[s] = ld_sh(pc[s]);  // the exact step may move x_ik
-            }
-        }
-    }
-    return go_cold;
-}
 
 // Sweep levels [La, Lb] of one phase.  Levels are taken in batches of U: in
 // the common case nothing moves, so the U levels' checks read only data
@@ -756,17 +1048,16 @@ __device__ __forceinline__ bool level_full(int L, uint32_t base0, unsigned char 
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const SlotGeom<S> &G,
                                       CtaConst &cc, TileSync &ts, WarpDuals *wd, int warp, int b,
-                                      int ihi, int klo, uint32_t &head, double &viol) {
+                                      int ihi, int klo, uint32_t &head, double &viol, int &nbatch) {
     if (La > Lb) return;
     constexpr int U = MP_BATCH;
     constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
     const TileDesc &T = cc.T;
     const int lane = threadIdx.x & 31;
     double xcr[S];
-    if (!ALIAS) {  // alias-free levels: x_ik is this thread's alone
-#pragma unroll
-        for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
-    }
+    // alias-free levels: x_ik is this thread's alone and lives in a register,
+    // loaded once the first batch's dependencies are met (the previous
+    // phase's last level may still write it in the predecessor warp)
 #ifdef MP_TRACE
     const bool tr = cc.trace != nullptr;
 #else
@@ -774,44 +1065,114 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #endif
     unsigned long long c_pred = 0, c_ring = 0, c_hot = 0, c_cold = 0, c_rel = 0, n_cold = 0;
     long long t0 = tr ? clock64() : 0, t1;
+    // predecessor: the previous warp of the band; for warp 0 of a later band,
+    // the previous band's last warp.  A batch
+    // [L, Le] waits until the predecessor has finished Le: by induction every
+    // earlier warp of the tile then has too, so the lattice neighbours of this
+    // warp's slots may sit in any earlier warp (32*S < b allowed) or band.
+    // (warp 0 of a later band polls the previous band's last warp remotely;
+    // the values it needs from there were forwarded into its own copies and
+    // fenced by their writers before they published progress.)
+    const int C = cc.C;
+    const bool has_pred = warp > 0 || cc.band > 0;
+    const bool xclu = warp == 0;  // predecessor lives in another CTA
     const int *pred_flag = &ts.done[warp > 0 ? warp - 1 : 0];
-    int pred_seen = warp > 0 ? ld_acquire(pred_flag) : 0x3fffffff;
-    int landed_seen = ld_acquire(&ts.landed);
+    const uint32_t pred_remote = xclu && has_pred ? mapa(smem_u32(&ts.done[cc.nwc - 1]), cc.band - 1) : 0u;
+    int pred_seen = !has_pred ? 0x3fffffff : xclu ? ld_acquire_cluster(pred_remote) : ld_acquire(pred_flag);
+    int landed_seen = landed_min(ts, C);
     const int jtop0 = T.ilo + klo;  // top j at level L is L - jtop0
-    for (int L = La; L <= Lb; L += U) {
+    // A batch [L, Le] waits until the predecessor finished Le - lead.  With
+    // lead = 0, by induction every earlier warp of the tile then reached
+    // Le - 1, so lattice neighbours may sit in any earlier warp or band.  When
+    // a warp's slot rows span at least a tile row (lw*S >= b) every neighbour is
+    // in this warp or the previous one and Le - 1 suffices (lead = 1; equal to
+    // Le for aligned batches, it only matters at a phase's last, short batch).
+    // (Staggering the batch ends by one level per warp was tried: no gain.)
+    const bool lead_band = cc.lw * S >= b;
+    const int lead = lead_band && !xclu ? 1 : 0;
+    for (int L = La; L <= Lb;) {
         const int Le = min(L + U - 1, Lb);
         const uint32_t base0 = (uint32_t)(L - T.Lbeg) * PER_LEVEL;
+#ifdef MP_TIMELINE
+        const long long tl0 = clock64();
+#endif
         // dependencies of the whole batch: predecessor done with Le-1; ring landed
 #ifndef MP_EXP_NOWAIT
-        if (pred_seen < Le - 1) pred_seen = wait_geq_v(pred_flag, Le - 1);
+        if (pred_seen < Le - lead)
+            pred_seen = xclu ? wait_geq_cluster(pred_remote, Le) : wait_geq_v(pred_flag, Le - lead);
 #endif
         if (tr) { t1 = clock64(); c_pred += t1 - t0; t0 = t1; }
         const int need = min(Le - jtop0, T.jhi) >> 4;
 #ifndef MP_EXP_NOWAIT
-        if (landed_seen < need) landed_seen = wait_geq_v(&ts.landed, need);
+        while (landed_seen < need) {
+            landed_seen = landed_min(ts, C);
+            if (landed_seen < need) spin_pause();
+        }
 #endif
         if (tr) { t1 = clock64(); c_ring += t1 - t0; t0 = t1; }
-        const int pf = warp > 0 ? ld_acquire(pred_flag) : 0x3fffffff;  // for the next batch
-        bool bad = false;
+#ifdef MP_TIMELINE
+        const long long tl1 = clock64();
+#endif
+        if (!ALIAS && L == La) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (L + u <= Le) {
+            for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
+        }
+        const int pf = !has_pred ? 0x3fffffff  // for the next batch
+                       : xclu ? ld_acquire_cluster(pred_remote) : ld_acquire(pred_flag);
+        unsigned fl = 0;  // bit u: level L+u has a violated row in some slot of this lane
+#ifndef MP_EXP_BRANCHY
+        if (Le - L + 1 == U) {
+#else
+        if (false) {
+#endif
+            // full batch: straight-line, so the U levels' loads overlap
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
                 int pa[S], pc[S], pe[S];
-                bad |= level_hot<S, W, ALIAS>(sm, G, L + u, b, ihi, klo, pa, pc, pe, xcr);
+                fl |= (unsigned)level_hot<S, W, ALIAS>(sm, G, L + u, b, ihi, klo, pa, pc, pe, xcr) << u;
+            }
+        } else {
+#pragma unroll 1
+            for (int Lx = L; Lx <= Le; ++Lx) {
+                int pa[S], pc[S], pe[S];
+                fl |= (unsigned)level_hot<S, W, ALIAS>(sm, G, Lx, b, ihi, klo, pa, pc, pe, xcr) << (Lx - L);
             }
         }
-        const bool wbad = __any_sync(0xffffffffu, bad);
+        const unsigned wfl = __reduce_or_sync(0xffffffffu, fl);
         const uint32_t lim = base0 + (uint32_t)(Le - L + 1) * PER_LEVEL;
-        const bool go_cold = wbad || head < lim;
+#ifndef MP_EXP_NOCOLD
+        const bool go_cold = wfl != 0u || head < lim;
+#else
+        const bool go_cold = false;  // timing experiment only: results are wrong
+#endif
         if (tr) { t1 = clock64(); c_hot += t1 - t0; t0 = t1; n_cold += go_cold; }
         if (go_cold) {
-            // first level of the batch that may need the exact step (level_full
-            // re-checks each level, so starting early is only slower)
-            int first = wbad ? L : Le + 1;
+            // first level that needs the exact step: flagged, or the next dual
+            int first = wfl ? L + __ffs(wfl) - 1 : Le + 1;
             if (head < lim) first = min(first, L + (int)((head - base0) / PER_LEVEL));
-            for (int Lc = first; Lc <= Le; ++Lc)
-                level_full<S, W, UNIT, ALIAS>(Lc, (uint32_t)(Lc - T.Lbeg) * PER_LEVEL, sm, G, cc,
-                                              wd, b, ihi, klo, xcr, head, viol);
+#ifdef MP_TIMELINE
+            if (lane == 0) wd->pad = nbatch;
+            __syncwarp();
+#endif
+            if (S == 1) {
+                viol = cold_batch<S, W, UNIT, ALIAS>(L, first, Le, wfl, &cc, wd, warp, viol);
+                head = wd->head;
+                if (!ALIAS) {  // the exact steps may have moved this thread's x_ik
+#pragma unroll
+                    for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
+                }
+            } else {
+                // level by level from `first`: skipped levels have no flag and
+                // no dual; after a replayed level every later one is re-checked
+                bool fwd = false, dirty = false;
+                for (int Lc = first; Lc <= Le; ++Lc) {
+                    const uint32_t bl = (uint32_t)(Lc - T.Lbeg) * PER_LEVEL;
+                    if (!dirty && !((wfl >> (Lc - L)) & 1u) && !(head < bl + PER_LEVEL)) continue;
+                    dirty |= level_full<S, W, UNIT, ALIAS>(Lc, bl, sm, G, &cc, wd, warp, b, ihi, klo, xcr,
+                                                           head, viol, fwd);
+                }
+                if (__any_sync(0xffffffffu, fwd)) fence_cluster();
+            }
         }
         if (tr) { t1 = clock64(); c_cold += t1 - t0; t0 = t1; }
         __syncwarp();
@@ -819,7 +1180,18 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
             if (go_cold) st_release(&ts.done[warp], Le);  // publishes the exact steps' writes
             else st_relaxed(&ts.done[warp], Le);
         }
+#ifdef MP_TIMELINE
+        if (cc.tl && lane == 0 && nbatch < TL_MAXB) {
+            unsigned long long *r = cc.trace + (((size_t)cc.band * 16 + warp) * TL_MAXB + nbatch) * TL_REC;
+            r[0] = (unsigned long long)tl0;
+            r[1] = (unsigned long long)tl1;
+            r[2] = (unsigned long long)clock64();
+            r[3] = go_cold ? 1ull : 0ull;
+        }
+#endif
+        ++nbatch;
         pred_seen = max(pred_seen, pf);
+        L = Le + 1;
         if (tr) { t1 = clock64(); c_rel += t1 - t0; t0 = t1; }
     }
     if (tr && lane == 0) {
@@ -848,9 +1220,13 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
     const int b = cc->b, lane = threadIdx.x & 31;
     const int ptid = threadIdx.x - nwc * 32, pn = np * 32;
     double *smd = reinterpret_cast<double *>(sm);
-    double *WR = smd, *WK = smd + b * W;
+    const int C = cc->C, band = cc->band;
+    const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
+    const bool last_band = band == C - 1;
+    double *WR = smd, *WK = smd + cc->RB * W;
     const int xsize = cc->xsize;
     const int blast = T.jhi / BLK;
+    const uint32_t band0_done = C > 1 ? mapa(smem_u32(&ts->done[0]), 0) : 0u;
     const int nres = W / BLK;
 #ifndef MP_LOOKAHEAD
 #define MP_LOOKAHEAD 4
@@ -870,6 +1246,8 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
                 fast = max(fast, __shfl_xor_sync(0xffffffffu, fast, o));
             }
             if (lane == 0) {
+                // load ahead of the cluster's fastest warp (band 0 leads)
+                if (C > 1) fast = max(fast, ld_acquire_cluster(band0_done) + 2 * MP_BATCH);
                 ts->pslow = slow + 1;  // next level of the slowest warp
                 ts->pfast = fast + 1;  // next level of the fastest warp
             }
@@ -880,7 +1258,7 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         bool busy = false;
         const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
         while (lo_res < low_need) {
-            ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, ptid, pn);
+            ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band);
             ++lo_res;
             busy = true;
         }
@@ -888,10 +1266,10 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         const int want = min(need_fast + LOOKAHEAD, blast);
         while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
             ++hi_issued;
-            ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn);
+            ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, true);
             if (!UNIT)
                 ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
-                                    WK + xsize, hi_issued, ptid, pn);
+                                    WK + xsize, hi_issued, ptid, pn, r0, r1, true);
             cp_async_commit();  // one group per block, same sequence in every thread
             busy = true;
         }
@@ -909,7 +1287,8 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
             if (now > landed) {
                 __threadfence_block();
                 producer_bar(pn);  // every producer thread's copies up to `now` landed
-                if (ptid == 0) st_release(&ts->landed, now);
+                if (ptid < C)  // every CTA of the cluster learns this band's landed block
+                    st_release_cluster(mapa(smem_u32(&ts->landed_by[band]), ptid), now);
                 landed = now;
                 busy = true;
             }
@@ -931,10 +1310,16 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const long long tk0 = clock64();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nt = blockDim.x, nwc = a.nwc, np = nt / 32 - nwc;  // compute / producer warps
-    const TileDesc T = a.tiles[blockIdx.x];
+    // a cluster of C CTAs shares one tile: CTA `band` owns rows [r0, r1) (relative to ilo)
+    const int C = (int)cluster_size();
+    const int band = C > 1 ? (int)cluster_rank() : 0;
+    const TileDesc T = a.tiles[blockIdx.x / C];
     const int b = a.b;
-    const int bb = b * b;
-    const SmemMap<W> M{b};
+    const int RB = (b + C - 1) / C;
+    const int r0 = band * RB, r1 = min(b, r0 + RB);
+    const bool last_band = band == C - 1;
+    const int64_t stream_base = T.stream0 + (int64_t)band * nwc;
+    const SmemMap<W> M{b, RB};
     // base aligned to W*8 bytes (the launch reserves the slack) so ring rows
     // are W*8-aligned shared addresses and a slot address is one LOP3
     unsigned char *sm = smem_raw + ((W * 8 - (smem_u32(smem_raw) & (W * 8 - 1))) & (W * 8 - 1));
@@ -961,28 +1346,40 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.dbg = a.dbg;
         cc.trace = a.trace;
         cc.kc = a.kc;
+        cc.C = C;
+        cc.band = band;
+        cc.RB = RB;
+        cc.nwc = nwc;
+        cc.rep_lo = (uint32_t)B32 + (uint32_t)M.wk();
+        cc.zero_lo = (uint32_t)B32 + (uint32_t)M.zero();
+        cc.rk_lo = (uint32_t)B32 + (uint32_t)M.rk();
+        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
+        cc.B32 = B32;
+        cc.lw = a.lw;
     }
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
     if (tid < 32) ts.done[tid] = T.Lbeg - 1;
 
     // --- staging prologue (all threads) -----------------------------------
-    rk_block<true>(T, b, a.ld, a.x, RK, tid, nt);
-    if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt);
+    rk_block<true>(T, b, a.ld, a.x, RK, tid, nt, 0, b);
+    if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt, 0, b);
     const int blast = T.jhi / BLK;
     const int lo0 = max(T.Lbeg - T.ihi - T.z, T.jlo) / BLK;
     const int hi0 = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
     for (int bk = lo0; bk <= hi0; ++bk) {
-        ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
+        ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, true);
         if (!UNIT)
             ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
-                                bk, tid, nt);
+                                bk, tid, nt, r0, r1, true);
     }
     cp_async_commit();
-    if (tid == 0) ts.landed = hi0;
+    if (tid < 16) ts.landed_by[tid] = hi0;  // every band lands the same prologue blocks
     WarpDuals *wd = wds + (warp < nwc ? warp : 0);
-    if (warp < nwc) rd_init(wd, a.rp, T.stream0 + warp, lane);
+    if (warp < nwc) rd_init(wd, a.rp, stream_base + warp, lane);
     cp_async_wait_all();
     __syncthreads();
+    // no CTA may forward into (or publish to) a CTA before its staging landed
+    if (C > 1) cluster_sync_all();
     const long long tk1 = clock64();
 
     double viol = 0.0;
@@ -991,44 +1388,47 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     } else {
         // --- per-slot geometry: q = warp*32*S + s*32 + lane -> (i,k) -------
         SlotGeom<S> G;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int q = warp * 32 * S + s * 32 + lane;
-            const int ii = q / b, kk = q - (q / b) * b;
-            const int i = T.ilo + ii, k = T.klo + kk;
-            const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
-            const bool ok = q < bb && i <= T.ihi && k <= T.z && js <= je;
-            G.ik8[s] = ok ? 8 * (i + k) : 0;
-            G.off[s] = ok ? i + k + js : 0x3fffffff;
-            G.span[s] = ok ? (unsigned)(je - js) : 0u;
-            G.pik[s] = B32 + (ok ? M.rk() + 8 * (ii * b + kk) : M.zero());
-            G.wr[s] = B32 + (ok ? M.wr() + ii * W * 8 : M.zero());
-            G.wk[s] = B32 + (ok ? M.wk() + kk * W * 8 : M.zero());
-            G.rkr[s] = B32 + (ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero());
-            G.rkc[s] = B32 + (ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero());
-        }
-        G.zero = B32 + M.zero();
+        slot_geom<S, W>(G, T, M, B32, b, r0, r1, warp, lane, a.lw);
         const int ihi = T.ihi, klo = T.klo;
         uint32_t head = wd->head;
         // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or
         // K) iff L in (2*ihi + z, 2*klo + ilo).
         const int mid_a = max(2 * ihi + T.z + 1, T.Lbeg);
         const int mid_b = min(2 * klo + T.ilo - 1, T.Lend);
+#ifdef MP_TIMELINE
+        if (cc.tl && warp == 0 && lane == 0) {
+            unsigned long long *r = cc.trace + (((size_t)band * 16 + 15) * TL_MAXB) * TL_REC;
+            r[0] = (unsigned long long)clock64();
+            r[1] = gtimer();
+        }
+#endif
+        int nbatch = 0;
         if (mid_a <= mid_b) {
-            sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
-            sweep<S, W, UNIT, false>(mid_a, mid_b, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
-            sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
+            sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
+            sweep<S, W, UNIT, false>(mid_a, mid_b, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
+            sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
         } else {
-            sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol);
+            sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
         }
     }
 
     // --- epilogue: write back everything still staged ----------------------
     __syncthreads();
+#ifdef MP_TIMELINE
+    if (cc.tl && tid == 0) {
+        unsigned long long *r = cc.trace + (((size_t)band * 16 + 15) * TL_MAXB) * TL_REC;
+        r[2] = (unsigned long long)clock64();
+        r[3] = gtimer();
+        r[4] = (unsigned long long)tk0;
+        r[5] = (unsigned long long)tk1;
+    }
+#endif
     const long long tk2 = clock64();
+    // own WR and RK rows (a row's final values live in its band); the last
+    // band holds the final WK (every band forwards its WK writes downstream)
     for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk)
-        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt);
-    rk_block<false>(T, b, a.ld, a.x, RK, tid, nt);
+        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band);
+    rk_block<false>(T, b, a.ld, a.x, RK, tid, nt, r0, r1);
 #ifdef MP_TRACE
     if (a.trace) {
         __syncthreads();
@@ -1042,15 +1442,18 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     }
 #endif
     if (warp < nwc) {
-        wr_finish(wd, a.wp, a.ctr, T.stream0 + warp, lane);
+        wr_finish(wd, a.wp, a.ctr, stream_base + warp, lane);
         viol = warp_max(viol);
         if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
     }
+    if (C > 1) cluster_sync_all();  // late remote stores must not hit an exited CTA
 }
 
 // dynamic shared memory of one CTA
-inline size_t tile_smem_bytes(int b, int W, bool unit, int nt) {
-    const size_t xb = W == 256 ? SmemMap<256>{b}.xbytes() : SmemMap<128>{b}.xbytes();
+inline size_t tile_smem_bytes(int b, int W, bool unit, int nt, int rb) {
+    const size_t xb = W == 512   ? SmemMap<512>{b, rb}.xbytes()
+                      : W == 256 ? SmemMap<256>{b, rb}.xbytes()
+                                 : SmemMap<128>{b, rb}.xbytes();
     return (size_t)W * 8 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
 }
 

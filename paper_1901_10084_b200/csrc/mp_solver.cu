@@ -205,9 +205,14 @@ struct mp_handle {
            *winvf = nullptr, *pu = nullptr, *pl = nullptr, *tmp = nullptr;
     double *snap_x = nullptr, *snap_f = nullptr, *snap_pu = nullptr, *snap_pl = nullptr;
 
-    // schedule
-    int S = 1, NT = 64, NWC = 1, NPW = 1, W = 128;
-    size_t smem = 0;
+    // schedule; per round a launch shape: C CTAs (a thread-block cluster) per
+    // tile, S slots per thread, NWC compute + NPW producer warps per CTA
+    struct RoundCfg {
+        int C = 1, S = 1, NWC = 1, NPW = 1, NT = 64, W = 128, RB = 1, LW = 32;
+        size_t smem = 0;
+    };
+    std::vector<RoundCfg> rcfg;       // per round
+    std::vector<int32_t> tile_round;  // round of each tile
     std::vector<TileDesc> tiles;
     std::vector<int64_t> round_off, round_cnt;
     std::vector<int64_t> tile_x;      // tile base x per tile (for dual decode)
@@ -297,30 +302,104 @@ int alloc_pool(mp_handle *h, int which, int32_t cap) {
     return MP_OK;
 }
 
-template <int S, int W, bool U>
-int launch_tiles_t(mp_handle *h, const TileArgs &a, int ntiles) {
-    auto k = tile_round_kernel<S, W, U>;
-    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
-    k<<<ntiles, h->NT, h->smem, h->st>>>(a);
-    CK(cudaGetLastError());
+using TileKernel = void (*)(TileArgs);
+
+template <int S>
+TileKernel tile_kernel_s(int W, bool unit) {
+    if (W == 256) return tile_round_kernel<S, 256, true>;  // W = 256 only for W = I
+    return unit ? tile_round_kernel<S, 128, true> : tile_round_kernel<S, 128, false>;
+}
+
+TileKernel tile_kernel_for(int S, int W, bool unit) {
+    if (W == 512) return S == 1 ? tile_round_kernel<1, 512, true> : tile_round_kernel<2, 512, true>;
+    switch (S) {
+        case 1: return tile_kernel_s<1>(W, unit);
+        case 2: return tile_kernel_s<2>(W, unit);
+        case 3: return tile_kernel_s<3>(W, unit);
+        case 4: return tile_kernel_s<4>(W, unit);
+        default: return tile_kernel_s<5>(W, unit);
+    }
+}
+
+cudaLaunchConfig_t tile_launch_config(const mp_handle::RoundCfg &c, int ntiles, cudaStream_t st,
+                                      cudaLaunchAttribute *attr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ntiles * c.C), 1, 1);
+    cfg.blockDim = dim3((unsigned)c.NT, 1, 1);
+    cfg.dynamicSmemBytes = c.smem;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)c.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c.C > 1 ? 1 : 0;
+    return cfg;
+}
+
+// One launch per round: ntiles tiles, C CTAs (one cluster) per tile.
+int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, int ntiles) {
+    TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = tile_launch_config(c, ntiles, h->st, attr);
+    CK(cudaLaunchKernelEx(&cfg, k, a));
     return MP_OK;
 }
 
-template <int S>
-int launch_tiles_s(mp_handle *h, const TileArgs &a, int ntiles) {
-    if (h->W == 256) return launch_tiles_t<S, 256, true>(h, a, ntiles);
-    return h->unit_x ? launch_tiles_t<S, 128, true>(h, a, ntiles)
-                     : launch_tiles_t<S, 128, false>(h, a, ntiles);
+// How many clusters of this shape the device can run at once (0 on error).
+int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
+    TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
+        return 0;
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = tile_launch_config(c, 1, h->st, attr);
+    int n = 0;
+    if (c.C == 1) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, c.NT, c.smem) != cudaSuccess) return 0;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return per_sm * sms;
+    }
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
-int launch_tiles(mp_handle *h, const TileArgs &a, int ntiles) {
-    switch (h->S) {
-        case 1: return launch_tiles_s<1>(h, a, ntiles);
-        case 2: return launch_tiles_s<2>(h, a, ntiles);
-        case 3: return launch_tiles_s<3>(h, a, ntiles);
-        case 4: return launch_tiles_s<4>(h, a, ntiles);
-        default: return launch_tiles_s<5>(h, a, ntiles);
-    }
+// Launch shape of a round with C CTAs per tile: the fewest slots per thread S
+// with at most 15 compute warps (any S is correct: a warp waits until its
+// predecessor finished the whole batch), up to 3 producer warps, W = 256
+// ring when it fits.
+mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
+    mp_handle::RoundCfg c;
+    const int b = h->b;
+    c.C = C;
+    c.RB = (b + C - 1) / C;
+    const int slots = c.RB * b;
+    int S = 1;
+    if (const char *e = getenv("MP_SLOTS")) S = std::max(S, atoi(e));
+    c.LW = 32;
+    if (const char *e = getenv("MP_LANES"))  // cluster rounds only (one CTA needs them all)
+        if (C > 1) c.LW = std::max(1, std::min(32, atoi(e)));
+    const int LW = c.LW;
+    while ((slots + LW * S - 1) / (LW * S) > MAX_CTA_THREADS / 32 - 1) ++S;
+    c.S = S;
+    c.NWC = (slots + LW * S - 1) / (LW * S);
+    c.NPW = std::min(3, MAX_CTA_THREADS / 32 - c.NWC);
+    if (const char *e = getenv("MP_PRODUCERS")) c.NPW = std::max(1, std::min(c.NPW, atoi(e)));
+    c.NT = 32 * (c.NWC + c.NPW);
+    // ring width: as many j-slots as fit (a cluster's bands drift apart by up
+    // to a few hundred levels; the ring bounds that drift)
+    c.W = 128;
+    if (h->unit_x && tile_smem_bytes(b, 256, true, c.NT, c.RB) <= 225 * 1024) c.W = 256;
+    if (h->unit_x && C > 1 && S <= 2 && tile_smem_bytes(b, 512, true, c.NT, c.RB) <= 225 * 1024) c.W = 512;
+    if (const char *e = getenv("MP_RING_W")) c.W = std::min(c.W, std::max(128, atoi(e)));
+    c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB);
+    return c;
 }
 
 int launch_pairs(mp_handle *h, const PairArgs &a) {
@@ -342,10 +421,9 @@ TileArgs tile_args(mp_handle *h) {
     ta.winvx = h->winvx;
     ta.ld = h->ld;
     ta.b = h->b;
-    ta.nt = h->NT;
-    ta.nwc = h->NWC;
     ta.kc = h->kc;
     ta.trace = h->trace;
+    ta.tl_round = getenv("MP_TL_ROUND") ? atoi(getenv("MP_TL_ROUND")) : -1;
     ta.eps = h->eps;
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[h->rp ^ 1];
@@ -393,7 +471,12 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     const int64_t cnt = h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r];
     if (!cnt) return MP_OK;
     ta.tiles = h->sh.on ? h->sh.d_my_tiles + h->sh.my_off[r] : h->d_tiles + h->round_off[r];
-    return launch_tiles(h, ta, (int)cnt);
+    const mp_handle::RoundCfg &c = h->rcfg[r];
+    ta.round_id = (int32_t)r;
+    ta.lw = c.LW;
+    ta.nt = c.NT;
+    ta.nwc = c.NWC;
+    return launch_tiles(h, c, ta, (int)cnt);
 }
 
 bool round_exchanges(const mp_handle *h, size_t r) {
@@ -542,14 +625,17 @@ struct Decoded {
     int64_t i, j, k, kind;
 };
 
+// w = the stream's index within its tile: band * NWC + warp
 Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
     const TileDesc &T = h->tiles[t];
-    const uint32_t per_level = (uint32_t)h->S * 96u;
+    const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[(size_t)t]];
+    const int band = w / c.NWC, wb = w % c.NWC;
+    const uint32_t per_level = (uint32_t)c.S * 96u;
     const uint32_t lvl = key / per_level, rem = key % per_level;
     const int s = (int)(rem / 96u), r2 = (int)(rem % 96u);
     const int lane = r2 / 3, kind = r2 % 3;
-    const int64_t q = (int64_t)w * 32 * h->S + (int64_t)s * 32 + lane;
-    const int64_t ii = q / h->b, kk = q % h->b;
+    const int64_t q = ((int64_t)wb * c.S + s) * c.LW + lane;
+    const int64_t ii = (int64_t)band * c.RB + q / h->b, kk = q % h->b;
     Decoded d;
     d.i = T.ilo + ii;
     d.k = T.klo + kk;
@@ -624,7 +710,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         std::memcpy(&bits, &h->eps, sizeof(bits));
         const bool all_ones = (bits & 0xFFFFFFFFFFFFFull) == 0xFFFFFFFFFFFFFull;
         h->kc.eps = h->eps;
-        h->kc.reps = (all_ones || getenv("MP_NO_FASTDIV")) ? 0.0 : 1.0 / h->eps;
+        const bool in_range = h->eps >= 0x1p-60 && h->eps <= 0x1p+60;  // see div_rn
+        h->kc.reps = (all_ones || !in_range || getenv("MP_NO_FASTDIV")) ? 0.0 : 1.0 / h->eps;
         h->kc.r3 = 1.0 / 3.0;
     }
 
@@ -641,23 +728,6 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         }
 
     // ---- schedule (schedule.tiled_rounds, schedule.py:117-153) -------------
-    {
-        // S slots per thread, NWC compute warps + 1 producer warp per CTA.
-        // b <= 32*S keeps every lattice neighbour in the same or previous warp.
-        int S = std::max(1, (b + 31) / 32);
-        while ((b * b + 32 * S - 1) / (32 * S) > MAX_CTA_THREADS / 32 - 1) ++S;
-        if (const char *e = getenv("MP_SLOTS")) S = std::max(S, atoi(e));
-        if (S > MAX_SLOTS) return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d needs too many slots", b));
-        h->S = S;
-        h->NWC = (b * b + 32 * S - 1) / (32 * S);
-        h->NPW = std::min(3, MAX_CTA_THREADS / 32 - h->NWC);  // producer warps
-        if (const char *e = getenv("MP_PRODUCERS")) h->NPW = std::max(1, std::min(h->NPW, atoi(e)));
-        h->NT = 32 * (h->NWC + h->NPW);
-    }
-    // ring width: 256 j-slots (16 blocks) when it fits, else 128
-    h->W = (h->unit_x && tile_smem_bytes(b, 256, true, h->NT) <= 225 * 1024) ? 256 : 128;
-    if (const char *e = getenv("MP_RING_W")) h->W = (atoi(e) == 256 && h->W == 256) ? 256 : 128;
-    const int nwarps = h->NWC;  // one dual stream per compute warp
     h->nib = (n + b - 1) / b + 2;
     h->nkb = (n - 1) / b + 2;
     h->tile_of_blk.assign((size_t)(h->nib * h->nkb), -1);
@@ -667,11 +737,11 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         for (int64_t c = 0; std::max<int64_t>(x + c * b, 0) + 2 <= z - c * b; ++c) {
             const int64_t tx = x + c * b, tz = z - c * b;
             TileDesc t = make_tile(tx, tz, b);
-            t.stream0 = (int64_t)h->tiles.size() * nwarps;
             const int64_t iblk = (t.ilo + b - 1) / b, kblk = (n - 1 - tz) / b;
             h->tile_of_blk[(size_t)(iblk * h->nkb + kblk)] = (int32_t)h->tiles.size();
             h->tiles.push_back(t);
             h->tile_x.push_back(tx);
+            h->tile_round.push_back((int32_t)h->round_cnt.size());
             ++cnt;
         }
         h->round_cnt.push_back(cnt);
@@ -679,16 +749,55 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     if (h->kind != MP_SCHEDULE_SERIAL) {
         for (int64_t z = n - 1; z >= 2; z -= b) emit(1 - b, z);
         for (int64_t x = 1; x + 2 <= n - 1; x += b) emit(x, n - 1);
-        h->nstreams = (int64_t)h->tiles.size() * nwarps;
-    } else {
-        h->nstreams = 3 * n * n;  // one stream per (level, row), serial_stream()
     }
-    for (const TileDesc &t : h->tiles) {
-        const uint64_t keys = (uint64_t)(t.Lend - t.Lbeg + 1) * (uint64_t)h->S * 96ull;
-        if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
+    // Launch shape per round: a round with few tiles spreads each tile over a
+    // cluster of C SMs (row bands, mp_device.cuh), as large as the device can
+    // co-schedule for all of the round's tiles at once.
+    {
+        const mp_handle::RoundCfg one = round_shape(h, 1);
+        if (h->kind != MP_SCHEDULE_SERIAL && (one.S > MAX_SLOTS || one.smem > 227 * 1024))
+            return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d does not fit one CTA", b));
+        int cmax = 8;
+        if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(8, atoi(e)));
+        std::vector<int> cap(9, -1);  // co-resident clusters per C (queried once)
+        for (size_t r = 0; r < h->round_cnt.size(); ++r) {
+            const int64_t cnt = h->round_cnt[r];
+            mp_handle::RoundCfg best = one;
+            for (int C = std::min(cmax, b); C >= 2 && cnt > 0; --C) {
+                const int RB = (b + C - 1) / C;
+                if ((C - 1) * RB >= b || cnt * C > prop.multiProcessorCount) continue;
+                const mp_handle::RoundCfg c = round_shape(h, C);
+                if (c.S > MAX_SLOTS || c.smem > 227 * 1024) continue;
+                if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
+                if (cap[C] >= cnt) {
+                    best = c;
+                    break;
+                }
+            }
+            h->rcfg.push_back(best);
+        }
+        if (getenv("MP_VERBOSE")) {
+            std::vector<int> hist(9, 0);
+            for (const auto &c : h->rcfg) hist[(size_t)c.C]++;
+            fprintf(stderr, "[mp] n=%lld b=%d rounds by cluster size:", (long long)n, b);
+            for (int C = 1; C <= 8; ++C)
+                if (hist[(size_t)C]) {
+                    const mp_handle::RoundCfg c = round_shape(h, C);
+                    fprintf(stderr, " C=%d:%d (S=%d NWC=%d NT=%d smem=%zu cap=%d)", C, hist[(size_t)C],
+                            c.S, c.NWC, c.NT, c.smem, C > 1 ? cap[(size_t)C] : -1);
+                }
+            fprintf(stderr, "\n");
+        }
+        int64_t acc = 0;  // one dual stream per (tile, band, compute warp)
+        for (size_t t = 0; t < h->tiles.size(); ++t) {
+            const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[t]];
+            h->tiles[t].stream0 = acc;
+            acc += (int64_t)c.C * c.NWC;
+            const uint64_t keys = (uint64_t)(h->tiles[t].Lend - h->tiles[t].Lbeg + 1) * (uint64_t)c.S * 96ull;
+            if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
+        }
+        h->nstreams = h->kind != MP_SCHEDULE_SERIAL ? acc : 3 * n * n;  // serial: (level, row)
     }
-    h->smem = tile_smem_bytes(b, h->W, h->unit_x, h->NT);
-    if (h->smem > 227 * 1024) return bail(fail(MP_ERR_UNSUPPORTED, "tile staging needs %zu bytes of shared memory", h->smem));
 
     int rc;
 #define TRY(call)                        \
@@ -938,7 +1047,6 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     if (h->nstreams)
         CK(cudaMemcpyAsync(hh.data(), P.head, hh.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    const int nwarps = h->NWC;
     const int64_t n = h->n;
     int64_t outpos = 0;
     struct E {
@@ -980,7 +1088,8 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     for (size_t t = 0; t < h->tiles.size(); ++t) {
         ents.clear();
         const int64_t tx = h->tile_x[t];
-        for (int w = 0; w < nwarps; ++w) {
+        const mp_handle::RoundCfg &rc = h->rcfg[(size_t)h->tile_round[t]];
+        for (int w = 0; w < rc.C * rc.NWC; ++w) {
             int32_t c = used ? hh[(size_t)(h->tiles[t].stream0 + w)] : -1;
             while (c >= 0 && c < used) {
                 for (int e = 0; e < CHUNK; ++e) {
@@ -1059,11 +1168,14 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         if (t < 0) return fail(MP_ERR_ARG, "key outside schedule");
         if (h->sh.on && h->sh.owner[(size_t)t] != h->sh.rank) continue;  // another shard's dual
         const TileDesc &T = h->tiles[(size_t)t];
-        const int64_t q = (i - T.ilo) * b + (k - T.klo);
-        const int64_t w = q / (32 * h->S), s = (q % (32 * h->S)) / 32, lane = q % 32;
+        const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[(size_t)t]];
+        const int64_t band = (i - T.ilo) / c.RB, S = c.S;
+        const int64_t q = (i - T.ilo - band * c.RB) * b + (k - T.klo);
+        const int64_t LW = c.LW;
+        const int64_t w = q / (LW * S), s = (q % (LW * S)) / LW, lane = q % LW;
         const int64_t lvl = i + j + k - T.Lbeg;
-        const uint32_t key32 = (uint32_t)(((lvl * h->S + s) * 96) + lane * 3 + kind);
-        ents.push_back({T.stream0 + w, {key32, vals[e]}});
+        const uint32_t key32 = (uint32_t)(((lvl * S + s) * 96) + lane * 3 + kind);
+        ents.push_back({T.stream0 + band * c.NWC + w, {key32, vals[e]}});
     }
     std::sort(ents.begin(), ents.end(), [](const auto &a, const auto &c) {
         return a.first != c.first ? a.first < c.first : a.second.first < c.second.first;
@@ -1156,16 +1268,21 @@ int mp_trace(mp_handle *h, int32_t enable, uint64_t *out, int32_t nslots) {
     g_err.clear();
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
+#ifdef MP_TIMELINE
+    const size_t ns = TL_SLOTS;  // diagnostic build: the per-batch timeline
+#else
+    const size_t ns = TR_NSLOTS;
+#endif
     if (enable && !h->trace) {
-        CK(cudaMalloc(&h->trace, TR_NSLOTS * sizeof(unsigned long long)));
-        CK(cudaMemsetAsync(h->trace, 0, TR_NSLOTS * sizeof(unsigned long long), h->st));
+        CK(cudaMalloc(&h->trace, ns * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(h->trace, 0, ns * sizeof(unsigned long long), h->st));
     }
     if (out && h->trace) {
-        unsigned long long buf[TR_NSLOTS];
-        CK(cudaMemcpyAsync(buf, h->trace, sizeof(buf), cudaMemcpyDeviceToHost, h->st));
+        std::vector<unsigned long long> buf(ns);
+        CK(cudaMemcpyAsync(buf.data(), h->trace, ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
-        for (int i = 0; i < nslots && i < TR_NSLOTS; ++i) out[i] = buf[i];
-        CK(cudaMemsetAsync(h->trace, 0, sizeof(buf), h->st));
+        for (size_t i = 0; i < (size_t)nslots && i < ns; ++i) out[i] = buf[i];
+        CK(cudaMemsetAsync(h->trace, 0, ns * sizeof(unsigned long long), h->st));
     }
     if (!enable && h->trace) {
         CK(cudaStreamSynchronize(h->st));
@@ -1326,7 +1443,9 @@ __global__ void check_div_kernel(double b, double rb, uint64_t seed, int64_t sam
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z ^= z >> 31;
-        const int ex = (int)((z >> 52) % 80) - 40;  // |a| in ~[2^-40, 2^40)
+        // |a| in ~[2^-40, 2^40), and every 16th sample across [2^-1000, 2^1000)
+        // (the fast path's edges and the IEEE fallback)
+        const int ex = (t & 15) == 0 ? (int)((z >> 52) % 2000) - 1000 : (int)((z >> 52) % 80) - 40;
         const double mant = __longlong_as_double((long long)((z & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
         double a = ldexp(mant, ex);
         if (z & (1ull << 63)) a = -a;
