@@ -205,3 +205,36 @@ def test_fast_division_is_ieee(divisor):
     _native.check(_native.load().mp_check_division(divisor, 20_000_000, 12345, _native.iptr(bad)),
                   "mp_check_division")
     assert bad[0] == 0
+
+
+@pytest.mark.parametrize("cluster,slots", [(1, None), (2, None), (3, None), (5, None), (8, None),
+                                           (4, 2), (8, 2), (6, 3)])
+@pytest.mark.parametrize("general_w", [False, True])
+def test_cluster_shapes_bitwise(oracle_lib, monkeypatch, cluster, slots, general_w):
+    """Every launch shape -- C CTAs per tile (row bands, DSMEM forwarding of
+    the replicated WK/RK), S slots per thread -- follows the reference order
+    bit for bit (MP_CLUSTER caps C; MP_SLOTS raises S)."""
+    monkeypatch.setenv("MP_CLUSTER", str(cluster))
+    if slots:
+        monkeypatch.setenv("MP_SLOTS", str(slots))
+    inst = instances.config_instance(1, n=180)
+    rx = rf = None
+    if general_w:
+        rng = np.random.default_rng(5)
+        rx = rng.uniform(0.5, 2.0, inst.npairs)
+        rf = rng.uniform(0.5, 2.0, inst.npairs)
+        inst.reg_x, inst.reg_f = rx, rf
+    sess = DeviceSession(inst, "tiled", 40)
+    ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, reg_x=rx, reg_f=rf,
+                                  b=40, workers=4)
+    for _ in range(4):
+        st = sess.run(1)[0]
+        rs = ref.run_pass()
+        assert st.max_violation == rs.max_violation
+    x, f = sess.state()
+    assert np.array_equal(x, ref.state()[0]) and np.array_equal(f, ref.state()[1])
+    keys, vals, _ = sess.duals()
+    rk, rv = ref.duals()
+    o1, o2 = np.argsort(keys), np.argsort(rk)
+    assert np.array_equal(keys[o1], rk[o2]) and np.array_equal(vals[o1], rv[o2])
+    sess.close()
