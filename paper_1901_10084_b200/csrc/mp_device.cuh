@@ -118,6 +118,7 @@ struct TileArgs {
     unsigned long long *trace;  // optional cycle counters (mp_trace), null = off
     int32_t round_id;           // schedule round of this launch
     int32_t lw;                 // active lanes per warp slot row (<= 32)
+    int32_t colm;               // column-major slot map in each band
     int32_t tl_round;           // MP_TIMELINE builds: round whose first tile is traced
 };
 
@@ -173,6 +174,7 @@ struct CtaConst {
     int32_t tl;           // MP_TIMELINE: this CTA records its timeline
     int32_t B32;          // shared address of the aligned staging base
     int32_t lw;           // active lanes per warp slot row
+    int32_t colm;         // column-major slot map (cluster bands)
     uint32_t rep_lo;      // shared address of WK (replicated in every band)
     uint32_t zero_lo;     // ... of the zero row (end of WK)
     uint32_t rk_lo;       // ... of RK
@@ -335,12 +337,30 @@ __device__ __forceinline__ void st_cluster_f64(uint32_t a, double v) {
 __device__ __forceinline__ void st_release_cluster(uint32_t a, int v) {
     asm volatile("st.release.cluster.shared::cluster.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire_cluster(uint32_t a) {
+__device__ __forceinline__ void st_relaxed_cluster(uint32_t a, int v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_cluster(uint32_t a) {
     int v;
-    asm volatile("ld.acquire.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    asm volatile("ld.relaxed.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+// Acquire of a flag in the cluster window.  Everything this kernel shares
+// across CTAs lives in shared memory, so the acquire is restricted to
+// shared::cluster (a plain ld.acquire.cluster also invalidates L1: CCTL.IVALL).
+__device__ __forceinline__ int ld_acquire_cluster(uint32_t a) {
+    int v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.b32 %0, [%1];\n\t"
+                 "fence.acquire.sync_restrict::shared::cluster.cluster;"
+                 : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+// Release of this thread's earlier remote (DSMEM) stores to the cluster.
+__device__ __forceinline__ void fence_cluster() {
+#ifndef MP_EXP_NOFENCE
+    asm volatile("fence.release.cluster;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -745,16 +765,23 @@ __device__ __forceinline__ bool level_hot(const unsigned char *sm, const SlotGeo
     return bad;
 }
 
-// Slot geometry of this thread: q = (warp*S + s)*lw + lane within the band
-// [r0, r1) of the tile, (i, k) = (ilo + r0 + q/b, klo + q%b); a warp may use
-// only lw < 32 lanes per slot row (less exact-step work per warp).
+// Slot geometry of this thread: slot q = (warp*S + s)*lw + lane within the
+// band [r0, r1) of the tile; row-major (i, k) = (ilo + r0 + q/b, klo + q%b),
+// or column-major in a cluster band (a warp then covers a few columns of all
+// the band's rows, so the warps of consecutive bands form a 2-D grid rather
+// than one long chain).  A warp may use only lw < 32 lanes per slot row.
 template <int S, int W>
 __device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, const SmemMap<W> &M,
-                                          int B32, int b, int r0, int r1, int warp, int lane, int lw) {
+                                          int B32, int b, int r0, int r1, int warp, int lane, int lw,
+                                          bool colm) {
+    const int rbc = r1 - r0;  // rows of this band
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const int q = (warp * S + s) * lw + lane;  // lanes >= lw idle (fewer slots per warp)
-        const int ii = r0 + q / b, kk = q - (q / b) * b;
+        // row-major: q = (i - ilo - r0)*b + (k - klo); column-major (cluster
+        // bands): q = (k - klo)*rbc + (i - ilo - r0)
+        const int ii = colm ? r0 + q % max(rbc, 1) : r0 + q / b;
+        const int kk = colm ? q / max(rbc, 1) : q - (q / b) * b;
         const int i = T.ilo + ii, k = T.klo + kk;
         const int js = max(i + 1, T.jlo), je = min(k - 1, T.jhi);
         const bool ok = lane < lw && q < (r1 - r0) * b && i <= T.ihi && k <= T.z && js <= je;
@@ -862,7 +889,7 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
     const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
     const SmemMap<W> M{b, cc->RB};
     SlotGeom<S> G;
-    slot_geom<S, W>(G, T, M, cc->B32, b, r0, r1, warp, lane, cc->lw);
+    slot_geom<S, W>(G, T, M, cc->B32, b, r0, r1, warp, lane, cc->lw, cc->colm);
     constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
     const int64_t stream = T.stream0 + (int64_t)band * cc->nwc + warp;
     const StepConsts k = cc->kc;
@@ -1000,9 +1027,12 @@ struct TileSync {
 // Lowest ring block landed in every CTA of the cluster: a block may be used
 // (and an upstream band may forward writes into it) only once every band's
 // copy of it has landed.
-__device__ __forceinline__ int landed_min(TileSync &ts, int C) {
-    int m = ld_acquire_cluster(smem_u32(&ts.landed_by[0]));
-    for (int d = 1; d < C; ++d) m = min(m, ld_acquire_cluster(smem_u32(&ts.landed_by[d])));
+// (Other bands' entries are back-pressure only -- this warp never reads their
+// rings -- so relaxed loads do; the own band's ring data is acquired.)
+__device__ __forceinline__ int landed_min(TileSync &ts, int C, int band) {
+    int m = ld_acquire(&ts.landed_by[band]);
+    for (int d = 0; d < C; ++d)
+        if (d != band) m = min(m, ld_relaxed_cluster(smem_u32(&ts.landed_by[d])));
     return m;
 }
 
@@ -1024,14 +1054,16 @@ __device__ __forceinline__ int wait_geq_v(const int *p, int v) {
     }
     return x;
 }
-// the same for a flag in another CTA of the cluster (shared::cluster address)
+// the same for a flag in another CTA of the cluster (shared::cluster
+// address): poll with relaxed loads (a cluster-scope acquire is expensive),
+// then one acquire of the value that satisfied the wait
 __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
-    int x = ld_acquire_cluster(a);
+    int x = ld_relaxed_cluster(a);
     while (x < v) {
         spin_pause();
-        x = ld_acquire_cluster(a);
+        x = ld_relaxed_cluster(a);
     }
-    return x;
+    return ld_acquire_cluster(a);
 }
 
 #ifndef MP_BATCH
@@ -1065,31 +1097,38 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #endif
     unsigned long long c_pred = 0, c_ring = 0, c_hot = 0, c_cold = 0, c_rel = 0, n_cold = 0;
     long long t0 = tr ? clock64() : 0, t1;
-    // predecessor: the previous warp of the band; for warp 0 of a later band,
-    // the previous band's last warp.  A batch
-    // [L, Le] waits until the predecessor has finished Le: by induction every
-    // earlier warp of the tile then has too, so the lattice neighbours of this
-    // warp's slots may sit in any earlier warp (32*S < b allowed) or band.
-    // (warp 0 of a later band polls the previous band's last warp remotely;
-    // the values it needs from there were forwarded into its own copies and
-    // fenced by their writers before they published progress.)
+    // Predecessors of this warp.  Row-major: the previous warp of the band,
+    // and for warp 0 of a later band the previous band's last warp.
+    // Column-major (cluster bands): the previous warp of the band (columns to
+    // the left) and, in the previous band, the warp holding the last row of
+    // this warp's rightmost column (so the warps form a 2-D grid: the chain
+    // from the tile's first warp to its last is C + nwc long, not C*nwc).
+    // A batch [L, Le] waits until each predecessor finished Le (- lead): by
+    // induction every warp holding a lattice predecessor of this warp's slots
+    // then reached Le - 1.  Remote flags are polled with cluster-scope
+    // acquires; the values this warp needs from there were forwarded into its
+    // own copies and fenced by their writers before those published progress.
     const int C = cc.C;
-    const bool has_pred = warp > 0 || cc.band > 0;
-    const bool xclu = warp == 0;  // predecessor lives in another CTA
-    const int *pred_flag = &ts.done[warp > 0 ? warp - 1 : 0];
-    const uint32_t pred_remote = xclu && has_pred ? mapa(smem_u32(&ts.done[cc.nwc - 1]), cc.band - 1) : 0u;
-    int pred_seen = !has_pred ? 0x3fffffff : xclu ? ld_acquire_cluster(pred_remote) : ld_acquire(pred_flag);
-    int landed_seen = landed_min(ts, C);
+    const int lwS = cc.lw * S;
+    const bool has_loc = warp > 0;
+    const int *loc_flag = &ts.done[warp > 0 ? warp - 1 : 0];
+    int rem_warp = cc.nwc - 1;
+    if (cc.colm) {
+        const int r0 = cc.band * cc.RB, rbc = max(1, min(b, r0 + cc.RB) - r0);
+        const int qmax = min(warp * lwS + lwS - 1, rbc * b - 1);
+        const int kmax = max(qmax, 0) / rbc;
+        rem_warp = min(cc.nwc - 1, (kmax * cc.RB + cc.RB - 1) / lwS);
+    }
+    const bool has_rem = cc.band > 0 && (cc.colm || warp == 0);
+    const uint32_t rem_flag = has_rem ? mapa(smem_u32(&ts.done[rem_warp]), cc.band - 1) : 0u;
+    // with whole tile rows per warp (lw*S >= b) and row-major slots every
+    // neighbour is in this warp or the previous one: Le - 1 suffices (equal
+    // to Le for aligned batches; it only matters at a phase's short batch)
+    const int lead = (!cc.colm && lwS >= b) ? 1 : 0;
+    int loc_seen = has_loc ? ld_acquire(loc_flag) : 0x3fffffff;
+    int rem_seen = has_rem ? ld_acquire_cluster(rem_flag) : 0x3fffffff;
+    int landed_seen = landed_min(ts, C, cc.band);
     const int jtop0 = T.ilo + klo;  // top j at level L is L - jtop0
-    // A batch [L, Le] waits until the predecessor finished Le - lead.  With
-    // lead = 0, by induction every earlier warp of the tile then reached
-    // Le - 1, so lattice neighbours may sit in any earlier warp or band.  When
-    // a warp's slot rows span at least a tile row (lw*S >= b) every neighbour is
-    // in this warp or the previous one and Le - 1 suffices (lead = 1; equal to
-    // Le for aligned batches, it only matters at a phase's last, short batch).
-    // (Staggering the batch ends by one level per warp was tried: no gain.)
-    const bool lead_band = cc.lw * S >= b;
-    const int lead = lead_band && !xclu ? 1 : 0;
     for (int L = La; L <= Lb;) {
         const int Le = min(L + U - 1, Lb);
         const uint32_t base0 = (uint32_t)(L - T.Lbeg) * PER_LEVEL;
@@ -1098,14 +1137,14 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #endif
         // dependencies of the whole batch: predecessor done with Le-1; ring landed
 #ifndef MP_EXP_NOWAIT
-        if (pred_seen < Le - lead)
-            pred_seen = xclu ? wait_geq_cluster(pred_remote, Le) : wait_geq_v(pred_flag, Le - lead);
+        if (loc_seen < Le - lead) loc_seen = wait_geq_v(loc_flag, Le - lead);
+        if (rem_seen < Le) rem_seen = wait_geq_cluster(rem_flag, Le);
 #endif
         if (tr) { t1 = clock64(); c_pred += t1 - t0; t0 = t1; }
         const int need = min(Le - jtop0, T.jhi) >> 4;
 #ifndef MP_EXP_NOWAIT
         while (landed_seen < need) {
-            landed_seen = landed_min(ts, C);
+            landed_seen = landed_min(ts, C, cc.band);
             if (landed_seen < need) spin_pause();
         }
 #endif
@@ -1117,8 +1156,13 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #pragma unroll
             for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
         }
-        const int pf = !has_pred ? 0x3fffffff  // for the next batch
-                       : xclu ? ld_acquire_cluster(pred_remote) : ld_acquire(pred_flag);
+        // progress seen now, for the next batch
+        const int lpf = has_loc ? ld_acquire(loc_flag) : 0x3fffffff;
+#ifdef MP_EXP_EAGER_REMOTE
+        const int rpf = has_rem ? ld_acquire_cluster(rem_flag) : 0x3fffffff;
+#else
+        const int rpf = 0;  // remote flags are read only when a wait needs them
+#endif
         unsigned fl = 0;  // bit u: level L+u has a violated row in some slot of this lane
 #ifndef MP_EXP_BRANCHY
         if (Le - L + 1 == U) {
@@ -1138,7 +1182,11 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
                 fl |= (unsigned)level_hot<S, W, ALIAS>(sm, G, Lx, b, ihi, klo, pa, pc, pe, xcr) << (Lx - L);
             }
         }
+#ifndef MP_EXP_VOTE
         const unsigned wfl = __reduce_or_sync(0xffffffffu, fl);
+#else
+        const unsigned wfl = __any_sync(0xffffffffu, fl != 0u) ? (1u << U) - 1u : 0u;
+#endif
         const uint32_t lim = base0 + (uint32_t)(Le - L + 1) * PER_LEVEL;
 #ifndef MP_EXP_NOCOLD
         const bool go_cold = wfl != 0u || head < lim;
@@ -1190,7 +1238,8 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
         }
 #endif
         ++nbatch;
-        pred_seen = max(pred_seen, pf);
+        loc_seen = max(loc_seen, lpf);
+        rem_seen = max(rem_seen, rpf);
         L = Le + 1;
         if (tr) { t1 = clock64(); c_rel += t1 - t0; t0 = t1; }
     }
@@ -1287,8 +1336,11 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
             if (now > landed) {
                 __threadfence_block();
                 producer_bar(pn);  // every producer thread's copies up to `now` landed
-                if (ptid < C)  // every CTA of the cluster learns this band's landed block
-                    st_release_cluster(mapa(smem_u32(&ts->landed_by[band]), ptid), now);
+                // every CTA of the cluster learns this band's landed block: the
+                // own CTA with a release (its warps read the ring), the others
+                // relaxed (back-pressure for their forwarded writes only)
+                if (ptid == band) st_release(&ts->landed_by[band], now);
+                else if (ptid < C) st_relaxed_cluster(mapa(smem_u32(&ts->landed_by[band]), ptid), now);
                 landed = now;
                 busy = true;
             }
@@ -1356,6 +1408,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
         cc.B32 = B32;
         cc.lw = a.lw;
+        cc.colm = a.colm;
     }
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
     if (tid < 32) ts.done[tid] = T.Lbeg - 1;
@@ -1388,7 +1441,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     } else {
         // --- per-slot geometry: q = warp*32*S + s*32 + lane -> (i,k) -------
         SlotGeom<S> G;
-        slot_geom<S, W>(G, T, M, B32, b, r0, r1, warp, lane, a.lw);
+        slot_geom<S, W>(G, T, M, B32, b, r0, r1, warp, lane, a.lw, a.colm != 0);
         const int ihi = T.ihi, klo = T.klo;
         uint32_t head = wd->head;
         // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or

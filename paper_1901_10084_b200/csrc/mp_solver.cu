@@ -209,6 +209,7 @@ struct mp_handle {
     // tile, S slots per thread, NWC compute + NPW producer warps per CTA
     struct RoundCfg {
         int C = 1, S = 1, NWC = 1, NPW = 1, NT = 64, W = 128, RB = 1, LW = 32;
+        bool colm = false;  // column-major slots in each band
         size_t smem = 0;
     };
     std::vector<RoundCfg> rcfg;       // per round
@@ -379,6 +380,8 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
     const int b = h->b;
     c.C = C;
     c.RB = (b + C - 1) / C;
+    c.colm = C > 1;
+    if (const char *e = getenv("MP_COLMAJOR")) c.colm = atoi(e) != 0;
     const int slots = c.RB * b;
     int S = 1;
     if (const char *e = getenv("MP_SLOTS")) S = std::max(S, atoi(e));
@@ -474,6 +477,7 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     const mp_handle::RoundCfg &c = h->rcfg[r];
     ta.round_id = (int32_t)r;
     ta.lw = c.LW;
+    ta.colm = c.colm ? 1 : 0;
     ta.nt = c.NT;
     ta.nwc = c.NWC;
     return launch_tiles(h, c, ta, (int)cnt);
@@ -635,7 +639,9 @@ Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
     const int s = (int)(rem / 96u), r2 = (int)(rem % 96u);
     const int lane = r2 / 3, kind = r2 % 3;
     const int64_t q = ((int64_t)wb * c.S + s) * c.LW + lane;
-    const int64_t ii = (int64_t)band * c.RB + q / h->b, kk = q % h->b;
+    const int64_t r0 = (int64_t)band * c.RB, rbc = std::max<int64_t>(1, std::min<int64_t>(h->b, r0 + c.RB) - r0);
+    const int64_t ii = c.colm ? r0 + q % rbc : r0 + q / h->b;
+    const int64_t kk = c.colm ? q / rbc : q % h->b;
     Decoded d;
     d.i = T.ilo + ii;
     d.k = T.klo + kk;
@@ -1170,7 +1176,8 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         const TileDesc &T = h->tiles[(size_t)t];
         const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[(size_t)t]];
         const int64_t band = (i - T.ilo) / c.RB, S = c.S;
-        const int64_t q = (i - T.ilo - band * c.RB) * b + (k - T.klo);
+        const int64_t r0 = band * c.RB, rbc = std::max<int64_t>(1, std::min<int64_t>(b, r0 + c.RB) - r0);
+        const int64_t q = c.colm ? (k - T.klo) * rbc + (i - T.ilo - r0) : (i - T.ilo - r0) * b + (k - T.klo);
         const int64_t LW = c.LW;
         const int64_t w = q / (LW * S), s = (q % (LW * S)) / LW, lane = q % LW;
         const int64_t lvl = i + j + k - T.Lbeg;
