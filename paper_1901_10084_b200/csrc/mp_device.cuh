@@ -152,9 +152,11 @@ struct alignas(16) WarpDuals {
     int32_t cur, pos;              // current buffer, first unconsumed entry
     int32_t has_next;              // buf[cur^1] holds (or receives) the next chunk
     uint32_t head;                 // key of the next unconsumed entry
-    int32_t wchunk, wfill;         // writer: current chunk (-1 none, -2 dead), fill
+    int32_t wchunk, wfill;         // writer: pool index of wbuf[wcur] (-1 none, -2 dead), fill
     uint32_t wcount;               // entries written by this warp
     int32_t pad;
+    ChunkRec wbuf[2];              // writer staging: the chunk being filled, the one in flight
+    int32_t wcur, wpad[3];
 };
 
 // Per-CTA constants, in shared memory (read by the out-of-line code).
@@ -434,8 +436,9 @@ __device__ __forceinline__ void rd_init(WarpDuals *w, const DualPool &p, int64_t
         w->cur = 0;
         w->pos = 0;
         w->wchunk = -1;
-        w->wfill = CHUNK;
+        w->wfill = 0;
         w->wcount = 0;
+        w->wcur = 0;
         mbar_fence_init();
     }
     __syncwarp();
@@ -515,6 +518,36 @@ __device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint3
 // ---------------------------------------------------------------------------
 // warp-stream writer: appends this pass's nonzero duals
 // ---------------------------------------------------------------------------
+// Entries are staged in a shared-memory chunk and a full chunk goes to the
+// pool with one bulk copy (cp.async.bulk, async proxy): no scattered global
+// stores on the exact-step path, and a later release fence does not wait for
+// them.  Two staging buffers: one filling, one possibly still being read by
+// its bulk copy.
+// every lane that wrote the staged chunk: make its writes visible to the
+// async proxy; then (after __syncwarp) one lane issues the copy
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                 "cp.async.bulk.commit_group;"
+                 ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One pool chunk index for this stream (lane 0; -1 on pool overflow).
+__device__ __forceinline__ int32_t wr_alloc(const DualPool &p, PassCounters *ctr) {
+    int32_t c = atomicAdd(&ctr->chunks_used, 1);
+    if (c >= p.cap) {
+        atomicExch(&ctr->overflow, 1);
+        c = -1;
+    }
+    return c;
+}
+
 __device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassCounters *ctr,
                                           int64_t stream, uint32_t base, int lane, double t0,
                                           double t1, double t2) {
@@ -523,51 +556,71 @@ __device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassC
     const unsigned m1 = __ballot_sync(0xffffffffu, h1);
     const unsigned m2 = __ballot_sync(0xffffffffu, h2);
     int32_t chunk = w->wchunk;
-    const int32_t fill = w->wfill;
     if ((m0 | m1 | m2) == 0u || chunk == -2) return;
-    const unsigned lt = (1u << lane) - 1u;
-    const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
-    const int total = __popc(m0) + __popc(m1) + __popc(m2);
-    const int nnew = (fill + total + CHUNK - 1) / CHUNK - 1;
-    int32_t c0 = 0;
-    if (nnew > 0) {
+    if (chunk == -1) {  // first entry of the stream: its first chunk
         if (lane == 0) {
-            c0 = atomicAdd(&ctr->chunks_used, nnew);
-            if (c0 + nnew > p.cap) {
-                atomicExch(&ctr->overflow, 1);
-                c0 = -1;
-            }
+            chunk = wr_alloc(p, ctr);
+            p.head[stream] = chunk >= 0 ? chunk : -1;
         }
-        c0 = __shfl_sync(0xffffffffu, c0, 0);
-        if (c0 < 0) {
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk < 0) {
             __syncwarp();
             if (lane == 0) w->wchunk = -2;
             __syncwarp();
             return;
         }
-        if (lane == 0) {
-            if (chunk >= 0) p.rec[chunk].next = c0;
-            else p.head[stream] = c0;
-        }
-        if (lane < nnew - 1) p.rec[c0 + lane].next = c0 + lane + 1;
     }
-    int e = fill + before;
+    const unsigned lt = (1u << lane) - 1u;
+    const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
+    const int total = __popc(m0) + __popc(m1) + __popc(m2);
+    int fill = w->wfill, cur = w->wcur;
+    // positions fill + before .. in key order (lane, kind); a position >= 32
+    // belongs to a later chunk: write the window, flush, move on
     const double th[3] = {t0, t1, t2};
     const bool hk[3] = {h0, h1, h2};
+    int start = 0;  // stream position of wbuf[cur][0], relative to this append
+    while (true) {
+        int e = fill + before;
 #pragma unroll
-    for (int kd = 0; kd < 3; ++kd) {
-        if (hk[kd]) {
-            const int blk = e / CHUNK;
-            const int32_t c = blk == 0 ? chunk : c0 + blk - 1;
-            p.rec[c].keys[e - blk * CHUNK] = base + 3u * (uint32_t)lane + (uint32_t)kd;
-            p.rec[c].vals[e - blk * CHUNK] = th[kd];
-            ++e;
+        for (int kd = 0; kd < 3; ++kd) {
+            if (hk[kd]) {
+                const int pos = e - start;
+                if (pos >= 0 && pos < CHUNK) {
+                    w->wbuf[cur].keys[pos] = base + 3u * (uint32_t)lane + (uint32_t)kd;
+                    w->wbuf[cur].vals[pos] = th[kd];
+                }
+                ++e;
+            }
         }
+        if (fill + total - start < CHUNK) break;
+        // wbuf[cur] is full: link it to a fresh chunk and send it
+        int32_t nxt = 0;
+        if (lane == 0) {
+            nxt = wr_alloc(p, ctr);
+            w->wbuf[cur].next = nxt;  // -1 on overflow: the pass is redone anyway
+        }
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            bulk_store(&p.rec[chunk], &w->wbuf[cur], sizeof(ChunkRec));
+            bulk_wait_read_le1();  // the other buffer's copy has read it
+        }
+        __syncwarp();
+        if (nxt < 0) {
+            if (lane == 0) w->wchunk = -2;
+            __syncwarp();
+            return;
+        }
+        chunk = nxt;
+        cur ^= 1;
+        start += CHUNK;
     }
     __syncwarp();
     if (lane == 0) {
-        w->wchunk = nnew > 0 ? c0 + nnew - 1 : chunk;
-        w->wfill = fill + total - CHUNK * nnew;
+        w->wchunk = chunk;
+        w->wcur = cur;
+        w->wfill = fill + total - start;
         w->wcount += (uint32_t)total;
     }
     __syncwarp();
@@ -575,14 +628,19 @@ __device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassC
 
 __device__ __forceinline__ void wr_finish(WarpDuals *w, const DualPool &p, PassCounters *ctr,
                                           int64_t stream, int lane) {
-    const int32_t chunk = w->wchunk, fill = w->wfill;
+    const int32_t chunk = w->wchunk, fill = w->wfill, cur = w->wcur;
     if (lane == 0 && w->wcount) atomicAdd(&ctr->nnz, (unsigned long long)w->wcount);
     if (chunk >= 0) {
-        if (lane >= fill) p.rec[chunk].keys[lane] = KEY_END;
-        if (lane == 0) p.rec[chunk].next = -1;
+        if (lane >= fill) w->wbuf[cur].keys[lane] = KEY_END;
+        if (lane == 0) w->wbuf[cur].next = -1;
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) bulk_store(&p.rec[chunk], &w->wbuf[cur], sizeof(ChunkRec));
     } else if (chunk == -1) {
         if (lane == 0) p.head[stream] = -1;
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
