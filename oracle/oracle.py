@@ -231,7 +231,27 @@ def tile_order(n, b, x, z):
                     yield (i, j, k)
 
 
+def cube_order(n, c):
+    """Serial order re-blocked into cubes of edge c: cube
+    levels in increasing block sum I+J+K (I <= J <= K), the cubes of a level
+    in any order (here: reversed, to show the order does not matter), and
+    inside a cube the triplets level by level in L = i+j+k."""
+    nb = (n + c - 1) // c
+    for s in range(3 * nb):
+        cubes = [(I, J, s - I - J) for I in range(nb) for J in range(I, nb)
+                 if J <= s - I - J < nb]
+        for (I, J, K) in reversed(cubes):
+            trip = [(i, j, k) for i in range(I * c, min(n, I * c + c))
+                    for j in range(max(J * c, i + 1), min(n, J * c + c))
+                    for k in range(max(K * c, j + 1), min(n, K * c + c))]
+            trip.sort(key=lambda t: (t[0] + t[1] + t[2], -t[0]))  # any order inside a level
+            yield from trip
+
+
 def visit_order(n, kind, b):
+    if kind == "cube":
+        yield from cube_order(n, b)
+        return
     if kind == "serial":
         for i in range(n - 2):
             for j in range(i + 1, n - 1):

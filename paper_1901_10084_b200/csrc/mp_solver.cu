@@ -25,7 +25,7 @@
 #include "metricproj_b200.h"
 #include "mp_aux.cuh"
 #include "mp_device.cuh"
-#include "mp_serial.cuh"
+#include "mp_cube.cuh"
 #include "mp_shard.cuh"
 
 using namespace mp;
@@ -214,6 +214,11 @@ struct mp_handle {
     };
     std::vector<RoundCfg> rcfg;       // per round
     std::vector<int32_t> tile_round;  // round of each tile
+    // schedule_kind "serial": the cube wavefront (mp_cube.cuh)
+    std::vector<CubeDesc> cubes;          // all cubes, by cube level
+    std::vector<int64_t> cube_off, cube_cnt;  // per cube level
+    CubeDesc *d_cubes = nullptr;
+    int64_t nb_cube = 0;                  // index blocks per axis
     std::vector<TileDesc> tiles;
     std::vector<int64_t> round_off, round_cnt;
     std::vector<int64_t> tile_x;      // tile base x per tile (for dual decode)
@@ -268,6 +273,7 @@ struct mp_handle {
             cudaFree(p.head);
         }
         cudaFree(d_tiles);
+        cudaFree(d_cubes);
         cudaFree(ctr);
         cudaFree(d_stats);
         cudaFree(d_scan);
@@ -450,20 +456,22 @@ int pass_begin(mp_handle *h) {
 }
 
 int pass_serial(mp_handle *h) {
-    SerialArgs sa{};
-    sa.x = h->x;
-    sa.winvx = h->winvx;
-    sa.ld = h->ld;
-    sa.n = (int32_t)h->n;
-    sa.eps = h->eps;
-    sa.rp = h->pool[h->rp];
-    sa.wp = h->pool[h->rp ^ 1];
-    sa.ctr = h->ctr;
-    sa.kc = h->kc;
-    const int grid = grid_for(h->n * 32, 256, 148 * 8);
-    for (int L = 3; L <= 3 * (int)h->n - 6; ++L) {
-        if (h->unit_x) serial_level_kernel<true><<<grid, 256, 0, h->st>>>(sa, L);
-        else serial_level_kernel<false><<<grid, 256, 0, h->st>>>(sa, L);
+    CubeArgs ca{};
+    ca.x = h->x;
+    ca.winvx = h->winvx;
+    ca.ld = h->ld;
+    ca.n = (int32_t)h->n;
+    ca.rp = h->pool[h->rp];
+    ca.wp = h->pool[h->rp ^ 1];
+    ca.ctr = h->ctr;
+    ca.kc = h->kc;
+    const size_t smem = cube_smem_bytes(h->unit_x);
+    auto k = h->unit_x ? cube_level_kernel<true> : cube_level_kernel<false>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (size_t s = 0; s < h->cube_cnt.size(); ++s) {
+        if (!h->cube_cnt[s]) continue;
+        ca.cubes = h->d_cubes + h->cube_off[s];
+        k<<<(unsigned)h->cube_cnt[s], CUBE_WARPS * 32, smem, h->st>>>(ca);
     }
     CK(cudaGetLastError());
     return MP_OK;
@@ -629,6 +637,17 @@ struct Decoded {
     int64_t i, j, k, kind;
 };
 
+// Index of cube (I, J, K), I <= J <= K, in h->cubes (cube levels in order,
+// inside a level I then J ascending).
+int64_t cube_index(const mp_handle *h, int64_t I, int64_t J, int64_t K) {
+    const int64_t sl = I + J + K, nb = h->nb_cube;
+    auto jlo = [&](int64_t i) { return std::max(i, sl - i - nb + 1); };  // J range of first index i
+    auto jhi = [&](int64_t i) { return (sl - i) / 2; };
+    int64_t t = h->cube_off[(size_t)sl];
+    for (int64_t i = 0; i < I; ++i) t += std::max<int64_t>(0, jhi(i) - jlo(i) + 1);
+    return t + (J - jlo(I));
+}
+
 // w = the stream's index within its tile: band * NWC + warp
 Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
     const TileDesc &T = h->tiles[t];
@@ -673,8 +692,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     if (!inst->d_flat || !inst->w_flat) return fail(MP_ERR_ARG, "d_flat / w_flat are required");
     if (cfg->schedule_kind < 0 || cfg->schedule_kind > 2)
         return fail(MP_ERR_ARG, "unknown schedule_kind %d", cfg->schedule_kind);
-    if (cfg->schedule_kind == MP_SCHEDULE_SERIAL && n > 8192)
-        return fail(MP_ERR_UNSUPPORTED, "schedule_kind 'serial' is limited to n <= 8192 on the device");
+    if (cfg->schedule_kind == MP_SCHEDULE_SERIAL && n > 20000)
+        return fail(MP_ERR_UNSUPPORTED, "schedule_kind 'serial' is limited to n <= 20000 on the device");
     const int b = cfg->schedule_kind == MP_SCHEDULE_DIAGONAL ? 1 : cfg->tile_b;
     if (b < 1) return fail(MP_ERR_ARG, "tile size must be >= 1, got %d", b);
     if (b > 48 && cfg->schedule_kind != MP_SCHEDULE_SERIAL)
@@ -802,7 +821,30 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
             const uint64_t keys = (uint64_t)(h->tiles[t].Lend - h->tiles[t].Lbeg + 1) * (uint64_t)c.S * 96ull;
             if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
         }
-        h->nstreams = h->kind != MP_SCHEDULE_SERIAL ? acc : 3 * n * n;  // serial: (level, row)
+        h->nstreams = acc;
+    }
+    if (h->kind == MP_SCHEDULE_SERIAL) {
+        // cube wavefront: cube levels s = I+J+K, I <= J <= K (mp_cube.cuh)
+        const int64_t nb = (n + CUBE_C - 1) / CUBE_C;
+        h->nb_cube = nb;
+        for (int64_t sl = 0; sl <= 3 * (nb - 1); ++sl) {
+            h->cube_off.push_back((int64_t)h->cubes.size());
+            int64_t cnt = 0;
+            for (int64_t I = 0; I < nb && 3 * I <= sl; ++I)
+                for (int64_t J = I; J < nb && I + 2 * J <= sl; ++J) {
+                    const int64_t K = sl - I - J;
+                    if (K < J || K >= nb) continue;
+                    CubeDesc cd{};
+                    cd.I = (int32_t)I;
+                    cd.J = (int32_t)J;
+                    cd.K = (int32_t)K;
+                    cd.stream0 = (int64_t)h->cubes.size() * CUBE_WARPS;
+                    h->cubes.push_back(cd);
+                    ++cnt;
+                }
+            h->cube_cnt.push_back(cnt);
+        }
+        h->nstreams = (int64_t)h->cubes.size() * CUBE_WARPS;
     }
 
     int rc;
@@ -818,6 +860,11 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->d_tiles, std::max<size_t>(h->tiles.size(), 1) * sizeof(TileDesc)));
     TRY(cudaMemcpyAsync(h->d_tiles, h->tiles.data(), h->tiles.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice, h->st));
+    if (!h->cubes.empty()) {
+        TRY(cudaMalloc(&h->d_cubes, h->cubes.size() * sizeof(CubeDesc)));
+        TRY(cudaMemcpyAsync(h->d_cubes, h->cubes.data(), h->cubes.size() * sizeof(CubeDesc),
+                            cudaMemcpyHostToDevice, h->st));
+    }
 
     // ---- instance and state --------------------------------------------------
     const size_t dense = (size_t)n * h->ld * sizeof(double);
@@ -858,7 +905,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->snap_pl, m * sizeof(double)));
 
     // ---- duals and bookkeeping -------------------------------------------------
-    const int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams / 4), 1 << 30);
+    const int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams / 4), 1 << 22);
     if ((rc = alloc_pool(h, 0, cap0))) return bail(rc);
     if ((rc = alloc_pool(h, 1, cap0))) return bail(rc);
     h->pair_grid = grid_for(m, 256, 148 * 8);
@@ -887,7 +934,8 @@ int64_t launches_per_pass(const mp_handle *h) {
         c += (h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r]) ? 1 : 0;
         if (round_exchanges(h, r)) c += 2;  // pack + unpack
     }
-    if (h->kind == MP_SCHEDULE_SERIAL) c += 3 * h->n - 8;
+    if (h->kind == MP_SCHEDULE_SERIAL)
+        for (int64_t cnt : h->cube_cnt) c += cnt ? 1 : 0;
     if (h->sh.on && h->sh.local && h->sh.world > 1 && h->sh.rank == 0) c += 1;  // counter reduce
     return c;
 }
@@ -1064,20 +1112,23 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     if (h->kind == MP_SCHEDULE_SERIAL) {
         // serial visit order is lexicographic (i, j, k, kind) = ascending key code
         std::vector<std::pair<int64_t, double>> all;
+        constexpr int c = CUBE_C, S = CUBE_S;
         for (int64_t s = 0; s < h->nstreams; ++s) {
-            const int L = (int)(s / n), i = (int)(s % n);
-            int klo, khi;
-            serial_krange((int)n, L, i, klo, khi);
-            if (L < 3 || klo > khi || 3 * i + 3 > L) continue;
-            int32_t c = used ? hh[(size_t)s] : -1;
-            while (c >= 0 && c < used) {
+            const CubeDesc &cd = h->cubes[(size_t)(s / CUBE_WARPS)];
+            const int64_t warp = s % CUBE_WARPS, Lmin = (int64_t)(cd.I + cd.J + cd.K) * c;
+            int32_t ch = used ? hh[(size_t)s] : -1;
+            while (ch >= 0 && ch < used) {
                 for (int e = 0; e < CHUNK; ++e) {
-                    const uint32_t key = hr[(size_t)c].keys[e];
+                    const uint32_t key = hr[(size_t)ch].keys[e];
                     if (key == KEY_END) break;
-                    const int64_t k = klo + key / 3, kind = key % 3, j = L - i - k;
-                    all.push_back({((i * n + j) * n + k) * 3 + kind, hr[(size_t)c].vals[e]});
+                    const int64_t lvl = key / (S * 96), rem = key % (S * 96);
+                    const int64_t sl = rem / 96, lane = (rem % 96) / 3, kind = rem % 3;
+                    const int64_t q = (warp * S + sl) * 32 + lane;
+                    const int64_t i = (int64_t)cd.I * c + q / c, k = (int64_t)cd.K * c + q % c;
+                    const int64_t j = Lmin + lvl - i - k;
+                    all.push_back({((i * n + j) * n + k) * 3 + kind, hr[(size_t)ch].vals[e]});
                 }
-                c = hr[(size_t)c].next;
+                ch = hr[(size_t)ch].next;
             }
         }
         std::sort(all.begin(), all.end());
@@ -1162,10 +1213,14 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         if (!(vals[e] > 0.0) || !std::isfinite(vals[e]))
             return fail(MP_ERR_ARG, "dual values must be positive and finite");
         if (h->kind == MP_SCHEDULE_SERIAL) {
-            const int L = (int)(i + j + k);
-            int klo, khi;
-            serial_krange((int)n, L, (int)i, klo, khi);
-            ents.push_back({serial_stream((int)n, L, (int)i), {(uint32_t)((k - klo) * 3 + kind), vals[e]}});
+            constexpr int c = CUBE_C, S = CUBE_S;
+            const int64_t I = i / c, J = j / c, K = k / c;
+            const int64_t ci = cube_index(h, I, J, K);
+            const int64_t q = (i - I * c) * c + (k - K * c);
+            const int64_t warp = q / (32 * S), sl = (q / 32) % S, lane = q % 32;
+            const int64_t lvl = i + j + k - (I + J + K) * c;
+            ents.push_back({h->cubes[(size_t)ci].stream0 + warp,
+                            {(uint32_t)((lvl * S + sl) * 96 + lane * 3 + kind), vals[e]}});
             continue;
         }
         const int64_t iblk = (i + b - 1) / b, kblk = (n - 1 - k) / b;

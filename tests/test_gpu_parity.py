@@ -165,7 +165,7 @@ def test_serial_schedule_bitwise(small_golden, n):
         assert np.max(np.abs(np.concatenate([x, f]) - g[f"dense_n{n}_v"])) <= 1e-10
 
 
-@pytest.mark.parametrize("n,reg", [(40, False), (77, True), (150, False)])
+@pytest.mark.parametrize("n,reg", [(40, False), (77, True), (150, False), (333, False), (260, True)])
 def test_serial_against_oracle(oracle_lib, n, reg):
     inst = instances.config_instance(1, n=n)
     rx = rf = None
