@@ -176,6 +176,16 @@ int mp_group_run_passes(mp_handle *const *hs, int32_t world, int32_t npasses, mp
 int mp_max_violation(int64_t n, const double *xv, const double *fv, const double *d_flat,
                      double *out);
 
+/* Correlation-clustering instance of a graph (instance.cc_instance,
+ * instance.py:124-161): closed-neighbourhood Jaccard J of every pair (the
+ * sparse product B*B^T on the device), s = log((1 + J - guard) / (1 - J +
+ * guard)) clipped to [-cap, cap] and pushed off zero by `offset`; d = 1 where
+ * s < 0 else 0, w = |s|, packed pair order.  The graph is CSR (rowptr[n+1],
+ * cols[rowptr[n]]: sorted neighbour lists, no self-loops).  d is exact; w
+ * matches numpy within the device log's accuracy (1 ulp). */
+int mp_cc_instance(int64_t n, const int64_t *rowptr, const int32_t *cols, double guard, double cap,
+                   double offset, double *d_flat, double *w_flat);
+
 /* Self-test of the device's fast exact division (Markstein step with a
  * precomputed reciprocal, used for the divisions by eps and by 3 in the metric
  * step): compares it with IEEE division on `samples` random dividends and

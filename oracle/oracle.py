@@ -307,3 +307,27 @@ def py_pass(n, eps, x, f, d_flat, winvx, winvf, duals, pair_duals, kind="tiled",
                 f[p] -= coef * winvf[p]
             pair_duals[p, row] = theta if theta > THETA_FLOOR else 0.0
     return viol, new
+
+
+# ---------------------------------------------------------------------------
+# instance construction (reference instance.py:124-161), numpy restatement
+# ---------------------------------------------------------------------------
+
+def cc_instance_np(rowptr, cols, n, offset=0.01, guard=0.05, cap=10.0):
+    """Packed (d, w) of the signed Jaccard instance: closed neighbourhoods
+    B (n x n, 0/1 with unit diagonal), inter = B B^T, union = |N[i]| + |N[j]|
+    - inter, J = inter/union, s = log((1 + J - guard)/(1 - J + guard)),
+    clip, offset away from 0; d = s < 0, w = |s| (instance.py:124-161)."""
+    B = np.zeros((n, n))
+    for u in range(n):
+        B[u, cols[rowptr[u]:rowptr[u + 1]]] = 1.0
+        B[u, u] = 1.0
+    inter = B @ B.T
+    sizes = B.sum(axis=1)
+    union = sizes[:, None] + sizes[None, :] - inter
+    J = inter / union
+    s = np.log((1.0 + J - guard) / (1.0 - J + guard))
+    np.clip(s, -cap, cap, out=s)
+    s = np.where(s >= 0, s + offset, s - offset)
+    iu = np.triu_indices(n, 1)
+    return np.where(s < 0, 1.0, 0.0)[iu], np.abs(s)[iu]

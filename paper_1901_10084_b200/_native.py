@@ -96,7 +96,7 @@ EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dua
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
            "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_check_division",
            "mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
-           "mp_group_run_passes", "mp_last_error", "mp_version")
+           "mp_group_run_passes", "mp_cc_instance", "mp_last_error", "mp_version")
 
 _lib = None
 
@@ -142,8 +142,10 @@ def load():
     L.mp_shard.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p]
     L.mp_group_run_passes.argtypes = [ctypes.POINTER(P), ctypes.c_int32, ctypes.c_int32,
                                       ctypes.POINTER(MPPassStats)]
+    L.mp_cc_instance.argtypes = [ctypes.c_int64, I, ctypes.POINTER(ctypes.c_int32), ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_double, D, D]
     for name in ("mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
-                 "mp_group_run_passes"):
+                 "mp_group_run_passes", "mp_cc_instance"):
         getattr(L, name).restype = ctypes.c_int
     L.mp_last_error.restype = ctypes.c_char_p
     L.mp_version.restype = ctypes.c_char_p

@@ -235,4 +235,52 @@ __global__ void reciprocal_kernel(const double *in, double *out, int64_t m) {
         out[p] = __ddiv_rn(1.0, in[p]);
 }
 
+// ---------------------------------------------------------------------------
+// correlation-clustering instance from a graph (instance.cc_instance,
+// instance.py:124-161)
+// ---------------------------------------------------------------------------
+// Closed-neighbourhood intersections |N[a] & N[b]| for a < b: node u adds 1
+// to every pair of N[u] = adj(u) + {u} (the sparse product B*B^T of the
+// reference, instance.py:124-139, one warp per node).
+__global__ void cc_inter_kernel(const int64_t *rowptr, const int32_t *cols, int64_t n,
+                                uint32_t *inter) {
+    const int lane = threadIdx.x & 31;
+    const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (u >= n) return;
+    const int64_t r0 = rowptr[u], deg = rowptr[u + 1] - r0, sz = deg + 1;
+    // element t of N[u]: the neighbours in order, then u itself
+    for (int64_t t = 0; t < sz; ++t) {
+        const int64_t a = t < deg ? cols[r0 + t] : u;
+        for (int64_t q = lane; q < sz; q += 32) {
+            const int64_t bq = q < deg ? cols[r0 + q] : u;
+            if (a < bq) atomicAdd(&inter[row_start(n, a) + (bq - a - 1)], 1u);
+        }
+    }
+}
+
+// J = inter / union, s = log((1 + J - guard) / (1 - J + guard)) clipped to
+// [-cap, cap] and pushed off zero by the offset; d = s < 0, w = |s|, packed
+// pair order -- numpy's elementwise operations in the same order
+// (instance.py:143-161).
+__global__ void cc_map_kernel(const uint32_t *inter, const int64_t *rowptr, int64_t n, int64_t m,
+                              double guard, double cap, double offset, double *d, double *w) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i, j;
+        unpack_pair(p, n, i, j);
+        const double in = (double)inter[p];
+        const double si = (double)(rowptr[i + 1] - rowptr[i] + 1);
+        const double sj = (double)(rowptr[j + 1] - rowptr[j] + 1);
+        const double un = __dsub_rn(__dadd_rn(si, sj), in);
+        const double J = __ddiv_rn(in, un);
+        const double num = __dsub_rn(__dadd_rn(1.0, J), guard);
+        const double den = __dadd_rn(__dsub_rn(1.0, J), guard);
+        double s = log(__ddiv_rn(num, den));
+        s = fmin(fmax(s, -cap), cap);
+        s = s >= 0.0 ? __dadd_rn(s, offset) : __dsub_rn(s, offset);
+        d[p] = s < 0.0 ? 1.0 : 0.0;
+        w[p] = fabs(s);
+    }
+}
+
 }  // namespace mp

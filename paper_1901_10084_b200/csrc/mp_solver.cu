@@ -1534,6 +1534,58 @@ int mp_check_division(double divisor, int64_t samples, uint64_t seed, int64_t *m
     return MP_OK;
 }
 
+int mp_cc_instance(int64_t n, const int64_t *rowptr, const int32_t *cols, double guard, double cap,
+                   double offset, double *d_flat, double *w_flat) {
+    g_err.clear();
+    if (n < 3) return fail(MP_ERR_ARG, "need at least 3 nodes, got %lld", (long long)n);
+    if (!(offset > 0.0)) return fail(MP_ERR_ARG, "sign offset must be positive, got %g", offset);
+    if (!rowptr || !d_flat || !w_flat || (rowptr[n] > 0 && !cols)) return fail(MP_ERR_ARG, "bad argument");
+    const int64_t nnz = rowptr[n];
+    for (int64_t u = 0; u < n; ++u)
+        if (rowptr[u + 1] < rowptr[u]) return fail(MP_ERR_ARG, "rowptr must be non-decreasing");
+    for (int64_t e = 0; e < nnz; ++e)
+        if (cols[e] < 0 || cols[e] >= n) return fail(MP_ERR_ARG, "neighbour index out of range");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MP_ERR_CUDA, "no CUDA device available; there is no CPU fallback");
+    const int64_t m = pair_count(n);
+    int64_t *drow = nullptr;
+    int32_t *dcol = nullptr;
+    uint32_t *inter = nullptr;
+    double *dd = nullptr, *dw = nullptr;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    auto cleanup = [&]() {
+        cudaFree(drow);
+        cudaFree(dcol);
+        cudaFree(inter);
+        cudaFree(dd);
+        cudaFree(dw);
+        cudaStreamDestroy(st);
+    };
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc(&drow, (size_t)(n + 1) * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&dcol, (size_t)std::max<int64_t>(nnz, 1) * sizeof(int32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&inter, (size_t)m * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&dd, (size_t)m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dw, (size_t)m * sizeof(double))) != cudaSuccess) {
+        cleanup();
+        return fail(MP_ERR_OOM, "cudaMalloc: %s", cudaGetErrorString(e));
+    }
+    cudaMemcpyAsync(drow, rowptr, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (nnz) cudaMemcpyAsync(dcol, cols, (size_t)nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(inter, 0, (size_t)m * sizeof(uint32_t), st);
+    cc_inter_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(drow, dcol, n, inter);
+    cc_map_kernel<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(inter, drow, n, m, guard, cap, offset, dd, dw);
+    cudaMemcpyAsync(d_flat, dd, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(w_flat, dw, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cleanup();
+    if (e != cudaSuccess) return fail(MP_ERR_CUDA, "cc_instance: %s", cudaGetErrorString(e));
+    return MP_OK;
+}
+
 int mp_max_violation(int64_t n, const double *xv, const double *fv, const double *d_flat,
                      double *out) {
     g_err.clear();

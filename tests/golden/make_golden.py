@@ -195,5 +195,47 @@ def main(which):
         save("small_cases", **small)
 
 
+def graph_edges(seed):
+    """Random edge lists with arbitrary node ids, a few duplicate and self-loop
+    lines and a second, smaller component (seeded; written as text)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(30, 160))
+    p = float(rng.uniform(0.03, 0.15))
+    ids = rng.permutation(10 * n)[:n] + 5
+    e = [(ids[a], ids[b]) for a in range(n) for b in range(a + 1, n) if rng.random() < p]
+    e += [e[t] for t in rng.integers(0, len(e), 3)]                # duplicates
+    e += [(ids[t], ids[t]) for t in rng.integers(0, n, 2)]         # self loops
+    base = 20 * n
+    e += [(base + t, base + t + 1) for t in range(5)]              # small component
+    rng.shuffle(e)
+    return np.array(e, dtype=np.int64)
+
+
+def graph_fixtures():
+    """The reference's instance pipeline (instance.load_edge_list ->
+    largest_component -> cc_instance) on seeded random edge lists."""
+    from metricproj import instance as rinstance
+    out = {}
+    for seed in (3, 4, 5):
+        edges = graph_edges(seed)
+        path = f"/tmp/golden_graph_{seed}.txt"
+        with open(path, "w") as fh:
+            fh.write("# seeded random graph\n")
+            for u, v in edges:
+                fh.write(f"{u} {v}\n")
+        g = rinstance.load_edge_list(path)
+        comp = rinstance.largest_component(g)
+        inst = rinstance.cc_instance(comp, epsilon=0.2)
+        out[f"s{seed}_edges"] = edges
+        out[f"s{seed}_n"] = np.array([g.n, comp.n, g.dropped_duplicates, g.dropped_self_loops])
+        out[f"s{seed}_labels"] = np.array(comp.labels, dtype=np.int64)
+        out[f"s{seed}_d"] = inst.d_flat
+        out[f"s{seed}_w"] = inst.w_flat
+    save("graphs", **out)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "small", "c2"])
+    which = sys.argv[1:] or ["c1", "small", "c2", "graphs"]
+    if "graphs" in which:
+        graph_fixtures()
+    main(which)
