@@ -51,7 +51,7 @@ inline size_t cube_smem_bytes(bool unit) {
 template <bool UNIT>
 __global__ void __launch_bounds__(CUBE_WARPS * 32, 2) cube_level_kernel(CubeArgs a) {
     constexpr int c = CUBE_C, S = CUBE_S, cc2 = CUBE_C * CUBE_C;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
     const CubeDesc cd = a.cubes[blockIdx.x];
     const int I = cd.I, J = cd.J, K = cd.K, n = a.n;
