@@ -940,14 +940,11 @@ __device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned
 #endif
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned flagged,
-                                          const CtaConst *cc, WarpDuals *wd, int warp, double viol) {
+                                          const CtaConst *cc, WarpDuals *wd, int warp, double viol,
+                                          const SlotGeom<S> G) {
     const int lane = threadIdx.x & 31;
     const TileDesc &T = cc->T;
     const int b = cc->b, C = cc->C, band = cc->band;
-    const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
-    const SmemMap<W> M{b, cc->RB};
-    SlotGeom<S> G;
-    slot_geom<S, W>(G, T, M, cc->B32, b, r0, r1, warp, lane, cc->lw, cc->colm);
     constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
     const int64_t stream = T.stream0 + (int64_t)band * cc->nwc + warp;
     const StepConsts k = cc->kc;
@@ -1261,7 +1258,7 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
             __syncwarp();
 #endif
             if (S == 1) {
-                viol = cold_batch<S, W, UNIT, ALIAS>(L, first, Le, wfl, &cc, wd, warp, viol);
+                viol = cold_batch<S, W, UNIT, ALIAS>(L, first, Le, wfl, &cc, wd, warp, viol, G);
                 head = wd->head;
                 if (!ALIAS) {  // the exact steps may have moved this thread's x_ik
 #pragma unroll
