@@ -139,9 +139,7 @@ __global__ void __launch_bounds__(CUBE_WARPS * 32, 2) cube_level_kernel(CubeArgs
                         wc = ld_sh(pc[s] + xb);
                         we = ld_sh(pe[s] + xb);
                     }
-                    double yq[3];
-                    rows_yq<UNIT>(y[0], wa, wc, we, k, yq);
-                    step3<UNIT>(p, cx, e, wa, wc, we, y[0], yq, k, viol, th);
+                    step3<UNIT>(p, cx, e, wa, wc, we, y[0], k, viol, th);
                     st_sh(pa[s], p);
                     st_sh(pc[s], cx);
                     st_sh(pe[s], e);

@@ -249,42 +249,7 @@ __device__ __forceinline__ bool row_step(double &p, double &m1, double &m2, doub
     return true;
 }
 
-// yq = (y*s)/eps of the three rows (kinds IJ, IK, JK), from the duals alone
-template <bool UNIT>
-__device__ __forceinline__ void rows_yq(const double (&y)[3], double wa, double wc, double we,
-                                        const StepConsts &k, double (&yq)[3]) {
-    const double s0 = row_s<UNIT>(wa, wc, we), s1 = row_s<UNIT>(wc, wa, we), s2 = row_s<UNIT>(we, wa, wc);
-    yq[0] = y[0] != 0.0 ? div_eps(__dmul_rn(y[0], s0), k) : 0.0;
-    yq[1] = y[1] != 0.0 ? div_eps(__dmul_rn(y[1], s1), k) : 0.0;
-    yq[2] = y[2] != 0.0 ? div_eps(__dmul_rn(y[2], s2), k) : 0.0;
-}
-
-// The three rows of triplet (i,j,k) in kind order IJ, IK, JK (_kernels.py:97-
-// 109), p = x_ij, c = x_ik, e = x_jk.  The row values are formed up front and
-// re-formed only after a row moved x, so each row sees exactly the value the
-// reference computes at its turn.  Returns whether x moved.
-template <bool UNIT>
-__device__ __forceinline__ bool step3(double &p, double &c, double &e, double wa, double wc,
-                                      double we, const double (&y)[3], const double (&yq)[3],
-                                      const StepConsts &k, double &viol, double (&th)[3]) {
-    double d0 = __dsub_rn(__dsub_rn(p, c), e);
-    double d1 = __dsub_rn(__dsub_rn(c, p), e);
-    double d2 = __dsub_rn(__dsub_rn(e, p), c);
-    bool moved = false;
-    if (row_step<UNIT>(p, c, e, wa, wc, we, y[0], yq[0], d0, k, viol, th[0])) {  // x_ij <= x_ik + x_jk
-        moved = true;
-        d1 = __dsub_rn(__dsub_rn(c, p), e);
-        d2 = __dsub_rn(__dsub_rn(e, p), c);
-    }
-    if (row_step<UNIT>(c, p, e, wc, wa, we, y[1], yq[1], d1, k, viol, th[1])) {  // x_ik <= x_ij + x_jk
-        moved = true;
-        d2 = __dsub_rn(__dsub_rn(e, p), c);
-    }
-    if (row_step<UNIT>(e, p, c, we, wa, wc, y[2], yq[2], d2, k, viol, th[2])) moved = true;  // x_jk
-    return moved;
-}
-
-// One row with everything formed in place (serial kernel).
+// One row, formed in place at its turn (_kernels.py:115-125).
 template <bool UNIT>
 __device__ __forceinline__ double dykstra_row(double &p, double &m1, double &m2, double wp,
                                               double wm1, double wm2, double y,
@@ -294,6 +259,17 @@ __device__ __forceinline__ double dykstra_row(double &p, double &m1, double &m2,
     double th;
     row_step<UNIT>(p, m1, m2, wp, wm1, wm2, y, yq, d0, k, viol, th);
     return th;
+}
+
+// The three rows of triplet (i,j,k) in kind order IJ, IK, JK (_kernels.py:97-
+// 109), p = x_ij, c = x_ik, e = x_jk, each formed from the current values.
+template <bool UNIT>
+__device__ __forceinline__ void step3(double &p, double &c, double &e, double wa, double wc,
+                                      double we, const double (&y)[3], const StepConsts &k,
+                                      double &viol, double (&th)[3]) {
+    th[0] = dykstra_row<UNIT>(p, c, e, wa, wc, we, y[0], k, viol);  // x_ij <= x_ik + x_jk
+    th[1] = dykstra_row<UNIT>(c, p, e, wc, wa, we, y[1], k, viol);  // x_ik <= x_ij + x_jk
+    th[2] = dykstra_row<UNIT>(e, p, c, we, wa, wc, y[2], k, viol);  // x_jk <= x_ij + x_ik
 }
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *addr, double v) {
@@ -888,9 +864,7 @@ __device__ __noinline__ double cold_slot(const CtaConst *cc, WarpDuals *wd, int 
             wc = ld_sh(pc + xb);
             we = ld_sh(pe + xb);
         }
-        double yq[3];
-        rows_yq<UNIT>(y[0], wa, wc, we, cc->kc, yq);
-        step3<UNIT>(p, c, e, wa, wc, we, y[0], yq, cc->kc, viol, th);
+        step3<UNIT>(p, c, e, wa, wc, we, y[0], cc->kc, viol, th);
         st_sh(pa, p);
         st_sh(pc, c);
         st_sh(pe, e);
@@ -985,9 +959,7 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
                               (y[0][0] != 0.0) | (y[0][1] != 0.0) | (y[0][2] != 0.0);
             bool any_th = false;
             if (need) {
-                double yq[3];
-                rows_yq<UNIT>(y[0], wa, wc, we, k, yq);
-                step3<UNIT>(p, c, e, wa, wc, we, y[0], yq, k, viol, th);
+                step3<UNIT>(p, c, e, wa, wc, we, y[0], k, viol, th);
                 st_sh(pa[s], p);
                 st_sh(pc[s], c);
                 st_sh(pe[s], e);
