@@ -112,7 +112,6 @@ struct TileArgs {
     double eps;
     DualPool rp, wp;
     PassCounters *ctr;
-    int32_t dbg;  // TEMP experiment switches
     int32_t nwc;  // compute warps per CTA (the rest are ring producers)
     StepConsts kc;
     unsigned long long *trace;  // optional cycle counters (mp_trace), null = off
@@ -170,7 +169,7 @@ struct CtaConst {
     PassCounters *ctr;
     unsigned long long *trace;
     StepConsts kc;
-    int32_t b, nt, xsize, dbg;
+    int32_t b, nt, xsize;
     int32_t C, band, RB;  // cluster size, this CTA's row band, rows per band
     int32_t nwc;          // compute warps per CTA
     int32_t tl;           // MP_TIMELINE: this CTA records its timeline
@@ -766,11 +765,7 @@ __device__ __forceinline__ void slot_addrs(const SlotGeom<S> &G, int L, int b, i
             pc[s] = act ? G.pik[s] : G.zero;
         } else {
             pa[s] = jm | G.wr[s];
-#ifndef MP_EXP_BCAST
             pe[s] = jm | G.wk[s];
-#else
-            pe[s] = G.zero;  // timing experiment: x_jk loads become broadcasts
-#endif
             pc[s] = G.pik[s];
         }
     }
@@ -1185,17 +1180,10 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
         }
         // progress seen now, for the next batch
         const int lpf = has_loc ? ld_acquire(loc_flag) : 0x3fffffff;
-#ifdef MP_EXP_EAGER_REMOTE
-        const int rpf = has_rem ? ld_acquire_cluster(rem_flag) : 0x3fffffff;
-#else
-        const int rpf = 0;  // remote flags are read only when a wait needs them
-#endif
+        // (remote flags are read only when a wait needs them: a remote load
+        // per batch costs more than it saves)
         unsigned fl = 0;  // bit u: level L+u has a violated row in some slot of this lane
-#ifndef MP_EXP_BRANCHY
         if (Le - L + 1 == U) {
-#else
-        if (false) {
-#endif
             // full batch: straight-line, so the U levels' loads overlap
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1209,11 +1197,7 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
                 fl |= (unsigned)level_hot<S, W, ALIAS>(sm, G, Lx, b, ihi, klo, pa, pc, pe, xcr) << (Lx - L);
             }
         }
-#ifndef MP_EXP_VOTE
         const unsigned wfl = __reduce_or_sync(0xffffffffu, fl);
-#else
-        const unsigned wfl = __any_sync(0xffffffffu, fl != 0u) ? (1u << U) - 1u : 0u;
-#endif
         const uint32_t lim = base0 + (uint32_t)(Le - L + 1) * PER_LEVEL;
 #ifndef MP_EXP_NOCOLD
         const bool go_cold = wfl != 0u || head < lim;
@@ -1266,7 +1250,6 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #endif
         ++nbatch;
         loc_seen = max(loc_seen, lpf);
-        rem_seen = max(rem_seen, rpf);
         L = Le + 1;
         if (tr) { t1 = clock64(); c_rel += t1 - t0; t0 = t1; }
     }
@@ -1422,7 +1405,6 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.b = b;
         cc.nt = nt;
         cc.xsize = xsize;
-        cc.dbg = a.dbg;
         cc.trace = a.trace;
         cc.kc = a.kc;
         cc.C = C;

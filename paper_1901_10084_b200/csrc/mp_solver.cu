@@ -437,7 +437,6 @@ TileArgs tile_args(mp_handle *h) {
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[h->rp ^ 1];
     ta.ctr = h->ctr;
-    ta.dbg = getenv("MP_DBG") ? atoi(getenv("MP_DBG")) : 0;
     return ta;
 }
 
