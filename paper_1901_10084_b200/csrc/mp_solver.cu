@@ -311,6 +311,7 @@ int alloc_pool(mp_handle *h, int which, int32_t cap) {
 
 using TileKernel = void (*)(TileArgs);
 
+
 template <int S>
 TileKernel tile_kernel_s(int W, bool unit) {
     if (W == 256) return tile_round_kernel<S, 256, true>;  // W = 256 only for W = I
@@ -410,6 +411,63 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
     c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB);
     return c;
 }
+
+// Launch shape per round: a round with few tiles spreads each tile over a
+// cluster of C SMs (row bands, mp_device.cuh), as large as the device can
+// co-schedule for all of the round's tiles at once (cnt[r] = tiles one
+// device runs in round r: all of them, or one rank's share when sharded).
+// Then one dual stream per (tile, band, compute warp), numbered in schedule
+// order.
+int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
+    const int b = h->b;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const mp_handle::RoundCfg one = round_shape(h, 1);
+    int cmax = 8;
+    if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(8, atoi(e)));
+    std::vector<int> cap(9, -1);  // co-resident clusters per C (queried once)
+    h->rcfg.clear();
+    for (size_t r = 0; r < cnt_r.size(); ++r) {
+        const int64_t cnt = cnt_r[r];
+        mp_handle::RoundCfg best = one;
+        for (int C = std::min(cmax, b); C >= 2 && cnt > 0; --C) {
+            const int RB = (b + C - 1) / C;
+            if ((C - 1) * RB >= b || cnt * C > sms) continue;
+            const mp_handle::RoundCfg c = round_shape(h, C);
+            if (c.S > MAX_SLOTS || c.smem > 227 * 1024) continue;
+            if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
+            if (cap[C] >= cnt) {
+                best = c;
+                break;
+            }
+        }
+        h->rcfg.push_back(best);
+    }
+    if (getenv("MP_VERBOSE")) {
+        std::vector<int> hist(9, 0);
+        for (const auto &c : h->rcfg) hist[(size_t)c.C]++;
+        fprintf(stderr, "[mp] n=%lld b=%d rounds by cluster size:", (long long)h->n, b);
+        for (int C = 1; C <= 8; ++C)
+            if (hist[(size_t)C]) {
+                const mp_handle::RoundCfg c = round_shape(h, C);
+                fprintf(stderr, " C=%d:%d (S=%d NWC=%d NT=%d smem=%zu cap=%d)", C, hist[(size_t)C], c.S,
+                        c.NWC, c.NT, c.smem, C > 1 ? cap[(size_t)C] : -1);
+            }
+        fprintf(stderr, "\n");
+    }
+    int64_t acc = 0;
+    for (size_t t = 0; t < h->tiles.size(); ++t) {
+        const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[t]];
+        h->tiles[t].stream0 = acc;
+        acc += (int64_t)c.C * c.NWC;
+        const uint64_t keys = (uint64_t)(h->tiles[t].Lend - h->tiles[t].Lbeg + 1) * (uint64_t)c.S * 96ull;
+        if (keys >= 0xFFFFFF00ull) return fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys");
+    }
+    h->nstreams = acc;
+    return MP_OK;
+}
+
 
 int launch_pairs(mp_handle *h, const PairArgs &a) {
     if (h->unit_x && h->unit_f)
@@ -774,53 +832,13 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         for (int64_t z = n - 1; z >= 2; z -= b) emit(1 - b, z);
         for (int64_t x = 1; x + 2 <= n - 1; x += b) emit(x, n - 1);
     }
-    // Launch shape per round: a round with few tiles spreads each tile over a
-    // cluster of C SMs (row bands, mp_device.cuh), as large as the device can
-    // co-schedule for all of the round's tiles at once.
-    {
+    // Launch shape per round and dual-stream numbering (plan_rounds)
+    if (h->kind != MP_SCHEDULE_SERIAL) {
         const mp_handle::RoundCfg one = round_shape(h, 1);
-        if (h->kind != MP_SCHEDULE_SERIAL && (one.S > MAX_SLOTS || one.smem > 227 * 1024))
+        if (one.S > MAX_SLOTS || one.smem > 227 * 1024)
             return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d does not fit one CTA", b));
-        int cmax = 8;
-        if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(8, atoi(e)));
-        std::vector<int> cap(9, -1);  // co-resident clusters per C (queried once)
-        for (size_t r = 0; r < h->round_cnt.size(); ++r) {
-            const int64_t cnt = h->round_cnt[r];
-            mp_handle::RoundCfg best = one;
-            for (int C = std::min(cmax, b); C >= 2 && cnt > 0; --C) {
-                const int RB = (b + C - 1) / C;
-                if ((C - 1) * RB >= b || cnt * C > prop.multiProcessorCount) continue;
-                const mp_handle::RoundCfg c = round_shape(h, C);
-                if (c.S > MAX_SLOTS || c.smem > 227 * 1024) continue;
-                if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
-                if (cap[C] >= cnt) {
-                    best = c;
-                    break;
-                }
-            }
-            h->rcfg.push_back(best);
-        }
-        if (getenv("MP_VERBOSE")) {
-            std::vector<int> hist(9, 0);
-            for (const auto &c : h->rcfg) hist[(size_t)c.C]++;
-            fprintf(stderr, "[mp] n=%lld b=%d rounds by cluster size:", (long long)n, b);
-            for (int C = 1; C <= 8; ++C)
-                if (hist[(size_t)C]) {
-                    const mp_handle::RoundCfg c = round_shape(h, C);
-                    fprintf(stderr, " C=%d:%d (S=%d NWC=%d NT=%d smem=%zu cap=%d)", C, hist[(size_t)C],
-                            c.S, c.NWC, c.NT, c.smem, C > 1 ? cap[(size_t)C] : -1);
-                }
-            fprintf(stderr, "\n");
-        }
-        int64_t acc = 0;  // one dual stream per (tile, band, compute warp)
-        for (size_t t = 0; t < h->tiles.size(); ++t) {
-            const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[t]];
-            h->tiles[t].stream0 = acc;
-            acc += (int64_t)c.C * c.NWC;
-            const uint64_t keys = (uint64_t)(h->tiles[t].Lend - h->tiles[t].Lbeg + 1) * (uint64_t)c.S * 96ull;
-            if (keys >= 0xFFFFFF00ull) return bail(fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys"));
-        }
-        h->nstreams = acc;
+        const int rc0 = plan_rounds(h, h->round_cnt);
+        if (rc0) return bail(rc0);
     }
     if (h->kind == MP_SCHEDULE_SERIAL) {
         // cube wavefront: cube levels s = I+J+K, I <= J <= K (mp_cube.cuh)
@@ -1406,6 +1424,27 @@ int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id) {
     std::vector<int64_t> tz;
     for (const TileDesc &t : h->tiles) tz.push_back(t.z);
     lpt_owner(h->b, world, h->tile_x, tz, h->round_cnt, S.owner);
+    // re-plan the launch shapes for the tiles one rank runs per round (the
+    // largest share over ranks, so every rank numbers the dual streams alike):
+    // fewer tiles per device leave room for larger clusters
+    if (world > 1) {
+        std::vector<int64_t> share(h->round_cnt.size(), 0);
+        for (size_t r = 0; r < h->round_cnt.size(); ++r) {
+            std::vector<int64_t> per((size_t)world, 0);
+            for (int64_t t = h->round_off[r]; t < h->round_off[r] + h->round_cnt[r]; ++t)
+                per[(size_t)S.owner[(size_t)t]]++;
+            share[r] = *std::max_element(per.begin(), per.end());
+        }
+        int rc = plan_rounds(h, share);
+        if (rc) return rc;
+        CK(cudaMemcpy(h->d_tiles, h->tiles.data(), h->tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+        for (auto &p : h->pool) {  // stream heads for the new numbering
+            cudaFree(p.head);
+            p.head = nullptr;
+            CK(cudaMalloc(&p.head, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
+            CK(cudaMemset(p.head, 0xff, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
+        }
+    }
     std::vector<TileDesc> mine;
     std::vector<FootDesc> foot(h->tiles.size());
     S.my_off.clear();
