@@ -443,6 +443,32 @@ __device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint3
     const uint32_t lim = base + (uint32_t)(S * 96);
     uint32_t head = w->head;
     int pos = w->pos, cur = w->cur;
+#ifndef MP_EXP_NOFASTLOOKUP
+    // common case: one entry in range, not the chunk's last -- broadcast reads
+    if (head < lim && pos + 1 < CHUNK) {
+        const uint32_t nxt = w->buf[cur].keys[pos + 1];
+        if (nxt >= lim) {
+            const double v = w->buf[cur].vals[pos];
+            const uint32_t off = head - base;
+            const uint32_t sl = off / 96u, r = off - 96u * sl;
+            if (r / 3u == (uint32_t)lane) {
+                const uint32_t kd = r - 3u * (uint32_t)lane;
+#pragma unroll
+                for (int ss = 0; ss < S; ++ss)
+#pragma unroll
+                    for (int kk = 0; kk < 3; ++kk)
+                        if (sl == (uint32_t)ss && kd == (uint32_t)kk) y[ss][kk] = v;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                w->head = nxt;
+                w->pos = pos + 1;
+            }
+            __syncwarp();
+            return;
+        }
+    }
+#endif
     while (head < lim) {
         const uint32_t key = w->buf[cur].keys[lane];
         const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && key < lim);
@@ -549,6 +575,20 @@ __device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassC
     const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
     const int total = __popc(m0) + __popc(m1) + __popc(m2);
     int fill = w->wfill, cur = w->wcur;
+    if (total == 1 && fill + 1 < CHUNK) {  // common case: one entry, room left
+        if (h0 | h1 | h2) {
+            w->wbuf[cur].keys[fill] = base + 3u * (uint32_t)lane + (h0 ? 0u : (h1 ? 1u : 2u));
+            w->wbuf[cur].vals[fill] = h0 ? t0 : (h1 ? t1 : t2);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            w->wchunk = chunk;
+            w->wfill = fill + 1;
+            w->wcount += 1u;
+        }
+        __syncwarp();
+        return;
+    }
     // positions fill + before .. in key order (lane, kind); a position >= 32
     // belongs to a later chunk: write the window, flush, move on
     const double th[3] = {t0, t1, t2};

@@ -34,6 +34,23 @@ print(f"pass {st.wall_time*1e3:.3f} ms")
 if a.dump:
     np.save(a.dump, v)
 bands = [c for c in range(8) if v[c, 15, 0, 0] != 0]
+if os.environ.get("TL_CRIT"):
+    # per band: sweep length, max warp work, mean wait; the warp with max work
+    for c in bands:
+        hdr = v[c, 15, 0]
+        works, waits, colds = [], [], []
+        for w in range(15):
+            r = v[c, w]
+            nb = int(np.count_nonzero(r[:, 2]))
+            if not nb:
+                continue
+            r = r[:nb]
+            works.append(int((r[:, 2] - r[:, 1]).sum()))
+            waits.append(int((r[:, 1] - r[:, 0]).sum()))
+            colds.append(int((r[:, 3] == 1).sum()))
+        print(f"band {c}: sweep {hdr[2]-hdr[0]:8d}  warps {len(works):2d}  max work {max(works):8d}  "
+              f"mean work {int(np.mean(works)):8d}  mean wait {int(np.mean(waits)):8d}  cold max {max(colds)}")
+    sys.exit(0)
 if os.environ.get("TL_SUMMARY"):
     for c in bands:
         r = v[c, :15].reshape(-1, 8)
