@@ -922,7 +922,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->snap_pl, m * sizeof(double)));
 
     // ---- duals and bookkeeping -------------------------------------------------
-    const int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams / 4), 1 << 22);
+    int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams / 4), 1 << 22);
+    if (const char *e = getenv("MP_POOL_CAP0")) cap0 = std::max(1, atoi(e));  // tests: force overflow
     if ((rc = alloc_pool(h, 0, cap0))) return bail(rc);
     if ((rc = alloc_pool(h, 1, cap0))) return bail(rc);
     h->pair_grid = grid_for(m, 256, 148 * 8);

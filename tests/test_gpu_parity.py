@@ -238,3 +238,26 @@ def test_cluster_shapes_bitwise(oracle_lib, monkeypatch, cluster, slots, general
     o1, o2 = np.argsort(keys), np.argsort(rk)
     assert np.array_equal(keys[o1], rk[o2]) and np.array_equal(vals[o1], rv[o2])
     sess.close()
+
+
+@pytest.mark.parametrize("kind,cluster", [("tiled", 8), ("tiled", 1), ("serial", 1)])
+def test_dual_pool_overflow_rolls_back(oracle_lib, monkeypatch, kind, cluster):
+    """A dual pool far too small: every pass overflows at first, is rolled
+    back from its snapshot and redone with a larger pool -- the trajectory
+    is unchanged (solver.run_pass semantics, bitwise vs the oracle)."""
+    monkeypatch.setenv("MP_POOL_CAP0", "2")
+    monkeypatch.setenv("MP_CLUSTER", str(cluster))
+    inst = instances.config_instance(1, n=120)
+    sess = DeviceSession(inst, kind, 40)
+    ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, kind=kind, b=40)
+    for _ in range(4):
+        st = sess.run(1)[0]
+        rs = ref.run_pass()
+        assert st.max_violation == rs.max_violation
+        assert st.nnz_metric == len(ref.duals()[0])
+    assert np.array_equal(sess.state()[0], ref.state()[0])
+    keys, vals, _ = sess.duals()
+    rk, rv = ref.duals()
+    o1, o2 = np.argsort(keys), np.argsort(rk)
+    assert np.array_equal(keys[o1], rk[o2]) and np.array_equal(vals[o1], rv[o2])
+    sess.close()
