@@ -961,7 +961,7 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
     const bool fwd_band = C > 1 && band + 1 < C;
     bool dirty = false, fwd = false;
 #ifdef MP_TIMELINE
-    long long tq0 = clock64(), c_lk = 0, c_mt = 0, c_ap = 0, nlev = 0;
+    long long tq0 = clock64(), c_lk = 0, c_mt = 0, c_ap = 0, c_ld = 0, nlev = 0;
 #endif
     for (int Lc = first; Lc <= Le; ++Lc) {
         const uint32_t base = (uint32_t)(Lc - T.Lbeg) * PER_LEVEL;
@@ -993,6 +993,9 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
             const bool need = (fabs(__dsub_rn(p, c)) > e) | (__dsub_rn(e, p) > c) |
                               (y[0][0] != 0.0) | (y[0][1] != 0.0) | (y[0][2] != 0.0);
             bool any_th = false;
+#ifdef MP_TIMELINE
+            { const long long t = clock64(); c_ld += t - tq; tq = t; }
+#endif
             if (need) {
                 step3<UNIT>(p, c, e, wa, wc, we, y[0], k, viol, th);
                 st_sh(pa[s], p);
@@ -1030,10 +1033,11 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
         const int nb = wd->pad;  // batch index parked by the caller
         if (nb < TL_MAXB) {
             unsigned long long *r = cc->trace + (((size_t)band * 16 + warp) * TL_MAXB + nb) * TL_REC;
-            r[4] = (unsigned long long)nlev;
-            r[5] = (unsigned long long)c_lk;
+            // lookup, x loads + check, exact step + stores + forwarding, append
+            r[4] = (unsigned long long)c_lk | ((unsigned long long)nlev << 48);
+            r[5] = (unsigned long long)c_ld;
             r[6] = (unsigned long long)c_mt;
-            r[7] = (unsigned long long)(clock64() - tq0 - c_lk - c_mt);
+            r[7] = (unsigned long long)c_ap | ((unsigned long long)(clock64() - tq0) << 32);
         }
     }
 #endif

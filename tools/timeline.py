@@ -57,9 +57,13 @@ if os.environ.get("TL_SUMMARY"):
         r = r[r[:, 2] != 0]
         cold = r[:, 3] == 1
         rc = r[cold]
-        print(f"band {c}: cold batches {cold.sum():4d}  cold batch {np.mean(rc[:,2]-rc[:,1]):6.0f}  levels "
-              f"{rc[:,4].mean():.2f}  lookup {rc[:,5].mean():5.0f}  math {rc[:,6].mean():5.0f}  rest {rc[:,7].mean():5.0f}  "
-              f"hot batch {np.mean(r[~cold,2]-r[~cold,1]):5.0f}")
+        lk = rc[:, 4] & ((1 << 48) - 1)
+        nl = rc[:, 4] >> 48
+        ap = rc[:, 7] & 0xFFFFFFFF
+        tot = rc[:, 7] >> 32
+        print(f"band {c}: cold batches {cold.sum():4d}  cold batch {np.mean(rc[:,2]-rc[:,1]):6.0f}  in call "
+              f"{tot.mean():6.0f} levels {nl.mean():.2f}  lookup {lk.mean():5.0f}  load+check {rc[:,5].mean():5.0f}  "
+              f"step {rc[:,6].mean():5.0f}  append {ap.mean():5.0f}  hot batch {np.mean(r[~cold,2]-r[~cold,1]):5.0f}")
     sys.exit(0)
 for c in bands:
     hdr = v[c, 15, 0]
