@@ -1466,6 +1466,11 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
     if (tid < 32) ts.done[tid] = T.Lbeg - 1;
 
+    // Programmatic dependent launch: everything above reads only this launch's
+    // arguments; x, the dual pools and the counters were written by the
+    // previous round, so wait for it here.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
     // --- staging prologue (all threads) -----------------------------------
     rk_block<true>(T, b, a.ld, a.x, RK, tid, nt, 0, b);
     if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt, 0, b);
@@ -1520,6 +1525,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 
     // --- epilogue: write back everything still staged ----------------------
     __syncthreads();
+    // the next round may launch (its CTAs wait in griddepcontrol.wait until
+    // this grid has finished and its writes are visible)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef MP_TIMELINE
     if (cc.tl && tid == 0) {
         unsigned long long *r = cc.trace + (((size_t)band * 16 + 15) * TL_MAXB) * TL_REC;

@@ -336,12 +336,21 @@ cudaLaunchConfig_t tile_launch_config(const mp_handle::RoundCfg &c, int ntiles, 
     cfg.blockDim = dim3((unsigned)c.NT, 1, 1);
     cfg.dynamicSmemBytes = c.smem;
     cfg.stream = st;
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)c.C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    int na = 0;
+    if (c.C > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)c.C;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (!getenv("MP_NO_PDL")) {  // programmatic dependent launch of consecutive rounds
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = c.C > 1 ? 1 : 0;
+    cfg.numAttrs = na;
     return cfg;
 }
 
@@ -349,7 +358,7 @@ cudaLaunchConfig_t tile_launch_config(const mp_handle::RoundCfg &c, int ntiles, 
 int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, int ntiles) {
     TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = tile_launch_config(c, ntiles, h->st, attr);
     CK(cudaLaunchKernelEx(&cfg, k, a));
     return MP_OK;
@@ -360,7 +369,7 @@ int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
     TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
         return 0;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = tile_launch_config(c, 1, h->st, attr);
     int n = 0;
     if (c.C == 1) {
