@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -354,10 +355,33 @@ cudaLaunchConfig_t tile_launch_config(const mp_handle::RoundCfg &c, int ntiles, 
     return cfg;
 }
 
+// Dynamic shared-memory opt-in of a kernel, set only when the size changes
+// (a cudaFuncSetAttribute per round costs host time).  Setting the maximum
+// once instead is much slower on the device (it changes the L1/shared split),
+// so the exact size is kept.
+int smem_optin(const void *k, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void *, int>, size_t>> cur;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (auto &e : cur)
+        if (e.first.first == k && e.first.second == dev) {
+            if (e.second != bytes) {
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+                e.second = bytes;
+            }
+            return MP_OK;
+        }
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur.push_back({{k, dev}, bytes});
+    return MP_OK;
+}
+
 // One launch per round: ntiles tiles, C CTAs (one cluster) per tile.
 int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, int ntiles) {
     TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
-    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+    if (int rc = smem_optin((const void *)k, c.smem)) return rc;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = tile_launch_config(c, ntiles, h->st, attr);
     CK(cudaLaunchKernelEx(&cfg, k, a));
@@ -367,8 +391,7 @@ int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, 
 // How many clusters of this shape the device can run at once (0 on error).
 int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
     TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem) != cudaSuccess)
-        return 0;
+    if (smem_optin((const void *)k, c.smem) != MP_OK) return 0;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = tile_launch_config(c, 1, h->st, attr);
     int n = 0;
@@ -931,7 +954,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->snap_pl, m * sizeof(double)));
 
     // ---- duals and bookkeeping -------------------------------------------------
-    int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams / 4), 1 << 22);
+    // about one chunk per stream: the first pass writes into most streams
+    int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams + h->nstreams / 4), 1 << 22);
     if (const char *e = getenv("MP_POOL_CAP0")) cap0 = std::max(1, atoi(e));  // tests: force overflow
     if ((rc = alloc_pool(h, 0, cap0))) return bail(rc);
     if ((rc = alloc_pool(h, 1, cap0))) return bail(rc);
@@ -993,8 +1017,11 @@ int run_group(std::vector<mp_handle *> &hs, int32_t npasses, mp_pass_stats *out)
         const int wp = h0->rp ^ 1;
         for (mp_handle *h : hs) {
             // keep the write pool comfortably above the last pass's usage
-            const int64_t want = std::max<int64_t>(h->pool[wp].cap, 2 * (int64_t)h->pool_used[h->rp] + 1024);
+            int64_t want = std::max<int64_t>(h->pool[wp].cap, 2 * (int64_t)h->pool_used[h->rp] + 1024);
             if (want > h->pool[wp].cap) {
+                // grow geometrically: a reallocation synchronises and costs ms
+                want = std::max<int64_t>(want, (int64_t)h->pool[wp].cap * 3 / 2);
+                if (getenv("MP_VERBOSE")) fprintf(stderr, "[mp] pool %d: %d -> %lld chunks\n", wp, h->pool[wp].cap, (long long)want);
                 CK(cudaStreamSynchronize(h->st));
                 int rc = alloc_pool(h, wp, (int32_t)std::min<int64_t>(want, 0x7fffffff));
                 if (rc) return rc;
@@ -1005,6 +1032,7 @@ int run_group(std::vector<mp_handle *> &hs, int32_t npasses, mp_pass_stats *out)
             if (rc) return rc;
             for (mp_handle *h : hs) CK(cudaStreamSynchronize(h->st));
             if (!h0->h_stats->overflow) break;  // all-reduced: every rank agrees
+            if (getenv("MP_VERBOSE")) fprintf(stderr, "[mp] pass %lld: dual pool overflow, redo\n", (long long)h0->pass_index);
             // dual pool overflow: roll the pass back, grow the pools, redo it
             for (mp_handle *h : hs) {
                 rc = restore_snapshot(h);
