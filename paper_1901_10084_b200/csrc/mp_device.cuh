@@ -356,6 +356,18 @@ __device__ __forceinline__ void st_sh(uint32_t a, double v) {
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async8s(uint32_t s, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(uint32_t s, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+// 16-byte shared -> global copy through registers
+__device__ __forceinline__ void st_global_v2(double *gp, uint32_t s) {
+    double a, c;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(c) : "r"(s) : "memory");
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(gp), "d"(a), "d"(c) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_2() { asm volatile("cp.async.wait_group 2;\n" ::); }
@@ -672,34 +684,60 @@ template <int W, bool LOAD>
 __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld, double *g,
                                            double *wr, double *wk, int blk, int tid, int nt,
                                            int r0, int r1, bool with_wk) {
+#ifdef MP_EXP_NOWB
+    if (!LOAD) return;  // timing experiment only: results are wrong
+#endif
+#ifdef MP_EXP_NOLOAD
+    return;  // timing experiment only: results are wrong
+#endif
     const int j0 = blk * BLK;
-    // WR: rows i in the band x 16 columns j (row-contiguous in global memory)
-    const int nwr = (r1 - r0) * BLK;
-    for (int e = tid; e < nwr; e += nt) {
-        const int ii = e / BLK, jj = e - ii * BLK;
-        const int i = T.ilo + r0 + ii, j = j0 + jj;
-        if (i <= T.ihi && j >= T.jlo && j <= T.jhi && j < T.klo && i < j) {
-            double *s = wr + ii * W + (j & (W - 1));
+    // WR: rows i in the band x 8 column pairs (j, j+1), j even: row-contiguous
+    // on both sides and 16-byte aligned (ld and W are multiples of 32), so an
+    // in-range pair is one 16-byte copy.  x_ij lives in WR iff
+    // jlo <= j <= min(jhi, klo - 1) and i < j.
+    {
+        const int wlo = T.jlo, whi = min(T.jhi, T.klo - 1);
+        const int nwr = (r1 - r0) * (BLK / 2);
+        for (int e = tid; e < nwr; e += nt) {
+            const int ii = e >> 3, j = j0 + ((e & 7) << 1);
+            const int i = T.ilo + r0 + ii;
+            const bool v0 = i <= T.ihi && j >= wlo && j <= whi && i < j;
+            const bool v1 = i <= T.ihi && j + 1 >= wlo && j + 1 <= whi && i < j + 1;
+            if (!(v0 | v1)) continue;
+            const uint32_t s = smem_u32(wr + ii * W + (j & (W - 1)));
             double *gp = g + (int64_t)i * ld + j;
-            if (LOAD) cp_async8(s, gp);
-            else *gp = *s;
+            if (v0 & v1) {
+                if (LOAD) cp_async16(s, gp);
+                else st_global_v2(gp, s);
+            } else {
+                if (LOAD) {
+                    if (v0) cp_async8s(s, gp);
+                    if (v1) cp_async8s(s + 8, gp + 1);
+                } else {
+                    if (v0) gp[0] = ld_sh(s);
+                    if (v1) gp[1] = ld_sh(s + 8);
+                }
+            }
         }
     }
     if (!with_wk) return;
-    // WK: 16 rows j x columns k in K; a warp covers 4 consecutive k (one
-    // 32-byte sector per row) x 8 rows j
+    // WK: 16 rows j x columns k in K (shared layout WK[k - klo][j % W]); a warp
+    // covers 4 consecutive k (one 32-byte sector per row) x 8 rows j; the
+    // warp-level loop keeps the index math to shifts and one compare.
+    // x_jk lives in WK iff jlo <= j <= jhi, j > ihi, j < k <= z.
     const int kq = (b + 3) / 4;
-    const int nwk = kq * 2 * 32;
-    for (int e = tid; e < nwk; e += nt) {
-        const int grp = e >> 5, ln = e & 31;
-        const int kk = (grp % kq) * 4 + (ln & 3);
-        const int jj = (grp / kq) * 8 + (ln >> 2);
-        const int k = T.klo + kk, j = j0 + jj;
-        if (kk < b && k <= T.z && j >= T.jlo && j <= T.jhi && j > T.ihi && j < k) {
-            double *s = wk + kk * W + (j & (W - 1));
+    const int lane = tid & 31, nw = nt >> 5;
+    const int jvlo = max(T.jlo, T.ihi + 1);
+    for (int t = tid >> 5; t < 2 * kq; t += nw) {
+        const int jh = t >= kq ? 1 : 0;
+        const int kk = (t - jh * kq) * 4 + (lane & 3);
+        const int j = j0 + jh * 8 + (lane >> 2);
+        const int k = T.klo + kk;
+        if (kk < b && k <= T.z && j >= jvlo && j <= T.jhi && j < k) {
+            const uint32_t s = smem_u32(wk + kk * W + (j & (W - 1)));
             double *gp = g + (int64_t)j * ld + k;
-            if (LOAD) cp_async8(s, gp);
-            else *gp = *s;
+            if (LOAD) cp_async8s(s, gp);
+            else *gp = ld_sh(s);
         }
     }
 }
@@ -1336,7 +1374,14 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
 #endif
     constexpr int LOOKAHEAD = MP_LOOKAHEAD;
     int landed = hi_issued;  // the prologue landed everything it issued
+#ifdef MP_TIMELINE
+    int nit = 0, nidle = 0;
+    unsigned long long *tlr = (cc->tl && ptid == 0) ? cc->trace + ((size_t)band * 16 + nwc) * TL_MAXB * TL_REC : nullptr;
+#endif
     while (true) {
+#ifdef MP_TIMELINE
+        const long long tp0 = clock64();
+#endif
         // Progress of every compute warp, each read with acquire so their ring
         // writes up to that level are visible.  Later warps may run ahead of
         // earlier ones (done[w] <= done[w-1] + 1 bounds them only from above).
@@ -1356,6 +1401,9 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
             }
         }
         producer_bar(pn);
+#ifdef MP_TIMELINE
+        const long long tp1 = clock64();
+#endif
         const int slow = ts->pslow, fast = ts->pfast;
         if (slow > T.Lend) break;
         bool busy = false;
@@ -1365,6 +1413,9 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
             ++lo_res;
             busy = true;
         }
+#ifdef MP_TIMELINE
+        const long long tp2 = clock64();
+#endif
         const int need_fast = min(fast - T.ilo - T.klo, T.jhi) / BLK;
         const int want = min(need_fast + LOOKAHEAD, blast);
         while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
@@ -1376,6 +1427,10 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
             cp_async_commit();  // one group per block, same sequence in every thread
             busy = true;
         }
+#ifdef MP_TIMELINE
+        const long long tp3 = clock64();
+        long long tp4 = tp3;
+#endif
         if (landed < hi_issued) {
             // publish what has landed; only wait for the newest copies when the
             // fastest warp is about to need them
@@ -1387,6 +1442,9 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
                 cp_async_wait_2();
                 now = hi_issued - 2;
             }
+#ifdef MP_TIMELINE
+            tp4 = clock64();
+#endif
             if (now > landed) {
                 __threadfence_block();
                 producer_bar(pn);  // every producer thread's copies up to `now` landed
@@ -1399,6 +1457,22 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
                 busy = true;
             }
         }
+#ifdef MP_TIMELINE
+        if (!busy) ++nidle;
+        if (tlr && busy && nit < TL_MAXB) {  // busy producer iteration (slot nwc of the band)
+            unsigned long long *r = tlr + (size_t)nit * TL_REC;
+            r[0] = (unsigned long long)tp0;
+            r[1] = (unsigned long long)tp1;
+            r[2] = (unsigned long long)tp2;
+            r[3] = (unsigned long long)tp3;
+            r[4] = (unsigned long long)tp4;
+            r[5] = (unsigned long long)clock64();
+            r[6] = ((unsigned long long)(unsigned)slow << 32) | (unsigned)fast;
+            r[7] = ((unsigned long long)(unsigned)lo_res << 48) | ((unsigned long long)(unsigned)hi_issued << 32) |
+                   ((unsigned long long)(unsigned)landed << 16) | (unsigned)min(nidle, 65535);
+            ++nit;
+        }
+#endif
         if (!busy) __nanosleep(32);
         producer_bar(pn);  // ts->pslow/pfast may be rewritten next round
     }

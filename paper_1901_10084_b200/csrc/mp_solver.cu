@@ -432,7 +432,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
     c.S = S;
     c.NWC = (slots + LW * S - 1) / (LW * S);
     c.NPW = std::min(3, MAX_CTA_THREADS / 32 - c.NWC);
-    if (const char *e = getenv("MP_PRODUCERS")) c.NPW = std::max(1, std::min(c.NPW, atoi(e)));
+    if (const char *e = getenv("MP_PRODUCERS")) c.NPW = std::max(1, std::min(MAX_CTA_THREADS / 32 - c.NWC, atoi(e)));
     c.NT = 32 * (c.NWC + c.NPW);
     // ring width: as many j-slots as fit (a cluster's bands drift apart by up
     // to a few hundred levels; the ring bounds that drift)
