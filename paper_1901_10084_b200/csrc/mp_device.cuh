@@ -179,7 +179,32 @@ struct CtaConst {
     uint32_t rep_lo;      // shared address of WK (replicated in every band)
     uint32_t zero_lo;     // ... of the zero row (end of WK)
     uint32_t rk_lo;       // ... of RK
+    uint32_t rk_row_mul;  // ceil(2^32 / (8b)): RK byte offset -> row (umulhi)
+    uint32_t band_mul;    // ceil(2^16 / RB): row -> band ((row * band_mul) >> 16)
 };
+
+// Forwarding of an exact step's x_jk write to the later bands that read it
+// (a cluster CTA's x_ij and x_ik lie in its own rows, which no later band
+// reads): a WK value is read by every later band, an RK value (row j of the
+// tile) by the later bands up to the owner of row j.  The remote stores are
+// independent, so they are unrolled (issued back to back).  Returns whether
+// anything was forwarded.
+__device__ __forceinline__ uint32_t mapa(uint32_t a, unsigned rank);
+__device__ __forceinline__ void st_cluster_f64(uint32_t a, double v);
+__device__ __forceinline__ bool forward_jk(const CtaConst *cc, uint32_t ue, double e) {
+    const int C = cc->C, band = cc->band;
+    int dlast = band;
+    if (ue >= cc->rep_lo && ue < cc->zero_lo) {
+        dlast = C - 1;
+    } else if (ue >= cc->rk_lo) {
+        const uint32_t row = __umulhi(ue - cc->rk_lo, cc->rk_row_mul);
+        dlast = min(C - 1, (int)((row * cc->band_mul) >> 16));
+    }
+#pragma unroll
+    for (int d = 1; d < 8; ++d)
+        if (band + d <= dlast) st_cluster_f64(mapa(ue, (unsigned)(band + d)), e);
+    return dlast > band;
+}
 
 // ---------------------------------------------------------------------------
 // one metric row, reference association (_kernels.py:115-125)
@@ -942,14 +967,7 @@ __device__ __noinline__ double cold_slot(const CtaConst *cc, WarpDuals *wd, int 
         st_sh(pc, c);
         st_sh(pe, e);
         const int C = cc->C, band = cc->band;
-        if (C > 1 && band + 1 < C) {  // forwarding rule: see cold_batch
-            const uint32_t ue = (uint32_t)pe;
-            int dlast = band;
-            if (ue >= cc->rep_lo && ue < cc->zero_lo) dlast = C - 1;
-            else if (ue >= cc->rk_lo) dlast = min(C - 1, (int)((ue - cc->rk_lo) / (8u * (uint32_t)cc->b)) / cc->RB);
-            for (int d = band + 1; d <= dlast; ++d) st_cluster_f64(mapa(ue, d), e);
-            fwd |= dlast > band;
-        }
+        if (C > 1 && band + 1 < C) fwd |= forward_jk(cc, (uint32_t)pe, e);
     }
     const int64_t stream = cc->T.stream0 + (int64_t)cc->band * cc->nwc + warp;
     if (__any_sync(0xffffffffu, (th[0] > THETA_FLOOR) | (th[1] > THETA_FLOOR) | (th[2] > THETA_FLOOR)))
@@ -1045,15 +1063,7 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
                 // rows i) and no later band (larger rows) reads those; x_jk is
                 // read later by every later band if it is in WK (j > ihi), and
                 // by the later bands up to the owner of row j if it is RK row j.
-                if (fwd_band) {
-                    const uint32_t ue = (uint32_t)pe[s];
-                    int dlast = band;
-                    if (ue >= cc->rep_lo && ue < cc->zero_lo) dlast = C - 1;
-                    else if (ue >= cc->rk_lo)
-                        dlast = min(C - 1, (int)((ue - cc->rk_lo) / (8u * (uint32_t)b)) / cc->RB);
-                    for (int d = band + 1; d <= dlast; ++d) st_cluster_f64(mapa(ue, d), e);
-                    fwd |= dlast > band;
-                }
+                if (fwd_band) fwd |= forward_jk(cc, (uint32_t)pe[s], e);
             }
 #ifdef MP_TIMELINE
             { const long long t = clock64(); c_mt += t - tq; tq = t; }
@@ -1171,7 +1181,7 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
 }
 
 #ifndef MP_BATCH
-#define MP_BATCH 4
+#define MP_BATCH 6
 #endif
 
 // Sweep levels [La, Lb] of one phase.  Levels are taken in batches of U: in
@@ -1532,6 +1542,8 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.rep_lo = (uint32_t)B32 + (uint32_t)M.wk();
         cc.zero_lo = (uint32_t)B32 + (uint32_t)M.zero();
         cc.rk_lo = (uint32_t)B32 + (uint32_t)M.rk();
+        cc.rk_row_mul = (uint32_t)((0x100000000ull + 8ull * (unsigned)b - 1) / (8ull * (unsigned)b));
+        cc.band_mul = (uint32_t)((65536u + (unsigned)RB - 1) / (unsigned)RB);
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
         cc.B32 = B32;
         cc.lw = a.lw;
