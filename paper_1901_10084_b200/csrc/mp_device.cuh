@@ -20,7 +20,7 @@
 //   RK[b][b]      every pair (a,c) with a in R and c in K  (canonical home,
 //                 so x_ij with j in K and x_jk with j in R alias into it)
 //   WR[b][W]      x_ij, i in R, j in J, j < klo  -- ring over j, slot j%W
-//   WK[b][W]      x_jk, j in J, j > ihi, k in K  -- ring over j, slot j%W
+//   WK[W][b]      x_jk, j in J, j > ihi, k in K  -- ring over j, row j%W
 // The rings are streamed from the dense (n x ld) x matrix in j-blocks of
 // BLK columns with cp.async one block ahead of the wavefront, and written
 // back when the wavefront has passed them.  Each pair touched by a tile is
@@ -119,6 +119,7 @@ struct TileArgs {
     int32_t lw;                 // active lanes per warp slot row (<= 32)
     int32_t colm;               // column-major slot map in each band
     int32_t tl_round;           // MP_TIMELINE builds: round whose first tile is traced
+    const void *tmap;           // 2-D TMA descriptor of x (box b x BLK), null: element copies
 };
 
 #ifdef MP_TIMELINE
@@ -181,6 +182,8 @@ struct CtaConst {
     uint32_t rk_lo;       // ... of RK
     uint32_t rk_row_mul;  // ceil(2^32 / (8b)): RK byte offset -> row (umulhi)
     uint32_t band_mul;    // ceil(2^16 / RB): row -> band ((row * band_mul) >> 16)
+    const void *tmap;     // TMA descriptor of x (WK blocks), or null
+    int32_t tma_st;       // the tile's K is b wide: interior WK blocks are stored by TMA
 };
 
 // Forwarding of an exact step's x_jk write to the later bands that read it
@@ -425,6 +428,27 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+// 2-D TMA box load into this CTA's shared memory, completing on `bar`
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void *tmap, int c0, int c1,
+                                            unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// 2-D TMA box store from this CTA's shared memory (bulk async-group)
+__device__ __forceinline__ void tma_store_2d(const void *tmap, int c0, int c1, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n\t"
+                 "cp.async.bulk.commit_group;" ::"l"(tmap),
+                 "r"(c0), "r"(c1), "r"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -746,23 +770,24 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld,
         }
     }
     if (!with_wk) return;
-    // WK: 16 rows j x columns k in K (shared layout WK[k - klo][j % W]); a warp
-    // covers 4 consecutive k (one 32-byte sector per row) x 8 rows j; the
-    // warp-level loop keeps the index math to shifts and one compare.
+    // WK: 16 rows j x columns k in K, shared layout WK[j % W][k - klo] (row
+    // pitch b, the same order as x, so a whole block is one 2-D TMA box; this
+    // element path serves the blocks TMA does not).  A warp takes one row j,
+    // lanes over k: contiguous on both sides.
     // x_jk lives in WK iff jlo <= j <= jhi, j > ihi, j < k <= z.
-    const int kq = (b + 3) / 4;
     const int lane = tid & 31, nw = nt >> 5;
     const int jvlo = max(T.jlo, T.ihi + 1);
-    for (int t = tid >> 5; t < 2 * kq; t += nw) {
-        const int jh = t >= kq ? 1 : 0;
-        const int kk = (t - jh * kq) * 4 + (lane & 3);
-        const int j = j0 + jh * 8 + (lane >> 2);
-        const int k = T.klo + kk;
-        if (kk < b && k <= T.z && j >= jvlo && j <= T.jhi && j < k) {
-            const uint32_t s = smem_u32(wk + kk * W + (j & (W - 1)));
-            double *gp = g + (int64_t)j * ld + k;
-            if (LOAD) cp_async8s(s, gp);
-            else *gp = ld_sh(s);
+    for (int rr = tid >> 5; rr < BLK; rr += nw) {
+        const int j = j0 + rr;
+        if (j < jvlo || j > T.jhi) continue;
+        const uint32_t srow = smem_u32(wk + (j & (W - 1)) * b);
+        double *grow = g + (int64_t)j * ld + T.klo;
+        for (int kk = lane; kk < b; kk += 32) {
+            const int k = T.klo + kk;
+            if (k <= T.z && j < k) {
+                if (LOAD) cp_async8s(srow + 8 * kk, grow + kk);
+                else grow[kk] = ld_sh(srow + 8 * kk);
+            }
         }
     }
 }
@@ -811,7 +836,8 @@ struct SlotGeom {
     unsigned span[S];
     int pik[S];       // byte offset of x_ik (RK) or of the zero row
     int wr[S];        // byte offset of WR row ii (or zero row)
-    int wk[S];        // byte offset of WK row kk (or zero row)
+    int wk[S];        // byte offset of WK column kk (or zero row)
+    int wkm[S];       // WK row pitch in doubles (b), 0 for an inactive slot
     int rkr[S];       // RK byte offset of x_ij when j in K:  rkr + 8j
     int rkc[S];       // RK byte offset of x_jk when j in R:  8*b*j + rkc
     int zero;         // shared address of the zero row
@@ -862,13 +888,13 @@ __device__ __forceinline__ void slot_addrs(const SlotGeom<S> &G, int L, int b, i
             const bool act = (unsigned)(L - G.off[s]) <= G.span[s];
             const int j = j8 >> 3;
             int a0 = j >= klo ? G.rkr[s] + j8 : (jm | G.wr[s]);
-            int e0 = j <= ihi ? j * (8 * b) + G.rkc[s] : (jm | G.wk[s]);
+            int e0 = j <= ihi ? j * (8 * b) + G.rkc[s] : jm * G.wkm[s] + G.wk[s];
             pa[s] = act ? a0 : G.zero;
             pe[s] = act ? e0 : G.zero;
             pc[s] = act ? G.pik[s] : G.zero;
         } else {
             pa[s] = jm | G.wr[s];
-            pe[s] = jm | G.wk[s];
+            pe[s] = jm * G.wkm[s] + G.wk[s];
             pc[s] = G.pik[s];
         }
     }
@@ -922,7 +948,8 @@ __device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, con
         G.span[s] = ok ? (unsigned)(je - js) : 0u;
         G.pik[s] = B32 + (ok ? M.rk() + 8 * (ii * b + kk) : M.zero());
         G.wr[s] = B32 + (ok ? M.wr() + (ii - r0) * W * 8 : M.zero());
-        G.wk[s] = B32 + (ok ? M.wk() + kk * W * 8 : M.zero());
+        G.wk[s] = B32 + (ok ? M.wk() + kk * 8 : M.zero());
+        G.wkm[s] = ok ? b : 0;
         G.rkr[s] = B32 + (ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero());
         G.rkc[s] = B32 + (ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero());
     }
@@ -1131,11 +1158,13 @@ __device__ __forceinline__ void wait_geq(const int *p, int v, bool sleep) {
 }
 
 struct TileSync {
+    unsigned long long wkbar[32];  // per WK ring block slot: its TMA load landed
     int done[32];       // last level each compute warp finished
     int landed_by[16];  // highest ring block landed, per CTA of the cluster
     int lo_res;         // producer's lowest resident block (for the epilogue)
     int hi_issued;      // producer's highest issued block (for the epilogue)
     int pslow, pfast;   // producer-internal broadcast
+    int blk0;           // the tile's first ring block (TMA slot phases count from it)
 };
 
 // Lowest ring block landed in every CTA of the cluster: a block may be used
@@ -1364,6 +1393,29 @@ __device__ __forceinline__ void producer_bar(int nthreads) {
     asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
 }
 
+// WK ring block g (rows j in [16g, 16g+16), columns K) as one 2-D TMA box;
+// slot barrier g % (W/BLK), phase ((g - blk0) / (W/BLK)) & 1 (blk0 = the
+// tile's first block, so every slot starts at phase 0).
+template <int W>
+__device__ __forceinline__ void wk_tma_load(const CtaConst *cc, TileSync *ts, double *WK, int g) {
+    unsigned long long *bar = &ts->wkbar[g & (W / BLK - 1)];
+    mbar_expect_tx(bar, (unsigned)(cc->b * BLK * 8));
+    tma_load_2d(smem_u32(WK + ((g * BLK) & (W - 1)) * cc->b), cc->tmap, cc->T.klo, g * BLK, bar);
+}
+template <int W>
+__device__ __forceinline__ void wk_tma_wait(TileSync *ts, int g) {
+    mbar_wait(&ts->wkbar[g & (W / BLK - 1)], (uint32_t)(((g - ts->blk0) / (W / BLK)) & 1));
+}
+// A WK block may be written back as a whole box when every row holds only
+// this tile's x_jk (j > ihi, j >= jlo; rows j >= z hold only k <= j pairs,
+// the unused lower triangle, written back unchanged) and K is b wide.
+__device__ __forceinline__ bool wk_tma_store_ok(const CtaConst *cc, int g) {
+    return cc->tmap != nullptr && cc->tma_st && g * BLK >= max(cc->T.jlo, cc->T.ihi + 1);
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 template <int W, bool UNIT>
 __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc, TileSync *ts,
                                            int nwc, int np, int lo_res, int hi_issued) {
@@ -1419,7 +1471,12 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         bool busy = false;
         const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
         while (lo_res < low_need) {
-            ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band);
+            const bool st = last_band && wk_tma_store_ok(cc, lo_res);
+            ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band && !st);
+            if (st && ptid == 0) {
+                fence_proxy_async();  // the compute warps' (acquired) writes, to the async proxy
+                tma_store_2d(cc->tmap, T.klo, lo_res * BLK, smem_u32(WK + ((lo_res * BLK) & (W - 1)) * b));
+            }
             ++lo_res;
             busy = true;
         }
@@ -1430,7 +1487,12 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         const int want = min(need_fast + LOOKAHEAD, blast);
         while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
             ++hi_issued;
-            ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, true);
+            ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, cc->tmap == nullptr);
+            if (cc->tmap && ptid == 0) {
+                bulk_wait_read_all();  // the slots' previous box store has read them
+                fence_proxy_async();
+                wk_tma_load<W>(cc, ts, WK, hi_issued);
+            }
             if (!UNIT)
                 ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
                                     WK + xsize, hi_issued, ptid, pn, r0, r1, true);
@@ -1452,6 +1514,8 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
                 cp_async_wait_2();
                 now = hi_issued - 2;
             }
+            if (cc->tmap)
+                for (int g = landed + 1; g <= now; ++g) wk_tma_wait<W>(ts, g);
 #ifdef MP_TIMELINE
             tp4 = clock64();
 #endif
@@ -1489,6 +1553,7 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
     if (ptid == 0) {
         ts->lo_res = lo_res;
         ts->hi_issued = hi_issued;
+        bulk_wait_all();  // box stores complete before the CTA exits
     }
 }
 
@@ -1510,6 +1575,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const bool last_band = band == C - 1;
     const int64_t stream_base = T.stream0 + (int64_t)band * nwc;
     const SmemMap<W> M{b, RB};
+    // TMA boxes need a 16-byte aligned start column: tiles with an odd klo copy
+    // WK element by element (the configs' even n give every tile an even klo)
+    const void *tmap = (T.klo & 1) ? nullptr : a.tmap;
     // base aligned to W*8 bytes (the launch reserves the slack) so ring rows
     // are W*8-aligned shared addresses and a slot address is one LOP3
     unsigned char *sm = smem_raw + ((W * 8 - (smem_u32(smem_raw) & (W * 8 - 1))) & (W * 8 - 1));
@@ -1544,6 +1612,8 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.rk_lo = (uint32_t)B32 + (uint32_t)M.rk();
         cc.rk_row_mul = (uint32_t)((0x100000000ull + 8ull * (unsigned)b - 1) / (8ull * (unsigned)b));
         cc.band_mul = (uint32_t)((65536u + (unsigned)RB - 1) / (unsigned)RB);
+        cc.tmap = tmap;
+        cc.tma_st = T.z - T.klo + 1 == b;
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
         cc.B32 = B32;
         cc.lw = a.lw;
@@ -1563,8 +1633,14 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const int blast = T.jhi / BLK;
     const int lo0 = max(T.Lbeg - T.ihi - T.z, T.jlo) / BLK;
     const int hi0 = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
+    if (tmap && tid == 0) {  // WK blocks by TMA (cc was written by this thread)
+        ts.blk0 = lo0;
+        for (int s = 0; s < W / BLK; ++s) mbar_init(&ts.wkbar[s], 1);
+        mbar_fence_init();
+        for (int bk = lo0; bk <= hi0; ++bk) wk_tma_load<W>(&cc, &ts, WK, bk);
+    }
     for (int bk = lo0; bk <= hi0; ++bk) {
-        ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, true);
+        ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, tmap == nullptr);
         if (!UNIT)
             ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
                                 bk, tid, nt, r0, r1, true);
@@ -1574,6 +1650,8 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     WarpDuals *wd = wds + (warp < nwc ? warp : 0);
     if (warp < nwc) rd_init(wd, a.rp, stream_base + warp, lane);
     cp_async_wait_all();
+    if (tmap && tid == 0)
+        for (int bk = lo0; bk <= hi0; ++bk) wk_tma_wait<W>(&ts, bk);
     __syncthreads();
     // no CTA may forward into (or publish to) a CTA before its staging landed
     if (C > 1) cluster_sync_all();
@@ -1626,8 +1704,14 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const long long tk2 = clock64();
     // own WR and RK rows (a row's final values live in its band); the last
     // band holds the final WK (every band forwards its WK writes downstream)
-    for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk)
-        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band);
+    for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk) {
+        const bool st = last_band && wk_tma_store_ok(&cc, bk);
+        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band && !st);
+        if (st && tid == 0) {  // wr_finish (warp 0) waits for the bulk group
+            fence_proxy_async();
+            tma_store_2d(tmap, T.klo, bk * BLK, smem_u32(WK + ((bk * BLK) & (W - 1)) * b));
+        }
+    }
     rk_block<false>(T, b, a.ld, a.x, RK, tid, nt, r0, r1);
 #ifdef MP_TRACE
     if (a.trace) {

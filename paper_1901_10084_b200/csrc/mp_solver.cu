@@ -9,6 +9,7 @@
 // phase + objective reductions -> a 1-CTA finalize -> ~64 bytes of stats to
 // pinned host memory.  The sparse dual pools are double-buffered: pass k
 // reads the pool pass k-1 wrote (SPEC.md "read pass k-1, write pass k").
+#include <cuda.h>  // CUtensorMap (the encoder is resolved through the runtime)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the functions are resolved at run time (nccl_api)
@@ -226,6 +227,7 @@ struct mp_handle {
     std::vector<int32_t> tile_of_blk; // (iblock, kblock) -> tile index
     int64_t nib = 0, nkb = 0;
     TileDesc *d_tiles = nullptr;
+    void *d_tmap = nullptr;  // 2-D TMA descriptor of x (WK ring blocks), null: element copies
     int64_t nstreams = 0;
 
     // sparse duals: two pools, pool[rp] holds the previous pass's duals
@@ -274,6 +276,7 @@ struct mp_handle {
             cudaFree(p.head);
         }
         cudaFree(d_tiles);
+        cudaFree(d_tmap);
         cudaFree(d_cubes);
         cudaFree(ctr);
         cudaFree(d_stats);
@@ -514,6 +517,40 @@ int launch_pairs(mp_handle *h, const PairArgs &a) {
     return MP_OK;
 }
 
+// 2-D TMA descriptor of the dense x (dims n x n, row pitch ld): WK ring blocks
+// (BLK rows j x b columns k) move as one box each.  Needs b * 8 bytes to be a
+// multiple of 16 (even b); otherwise (or with MP_NO_TMA) the tile kernel
+// copies WK element by element.  The encoder comes from the driver through
+// cudaGetDriverEntryPoint (no link-time libcuda dependency).
+typedef CUresult (*encode_tiled_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int make_x_tmap(mp_handle *h) {
+    if (h->kind != 2 || (h->b & 1) || h->b > 256 || getenv("MP_NO_TMA")) return MP_OK;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+        cudaGetLastError();
+        return MP_OK;  // no encoder: element copies
+    }
+    CUtensorMap map;
+    // inner extent ld (not n): with an odd n the box loads fault at the row end
+    const cuuint64_t dims[2] = {(cuuint64_t)h->ld, (cuuint64_t)h->n};
+    const cuuint64_t strides[1] = {(cuuint64_t)h->ld * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)h->b, (cuuint32_t)BLK};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = ((encode_tiled_fn)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->x, dims, strides,
+                                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    CK(cudaMalloc(&h->d_tmap, sizeof(CUtensorMap)));
+    CK(cudaMemcpy(h->d_tmap, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    return MP_OK;
+}
+
 TileArgs tile_args(mp_handle *h) {
     TileArgs ta{};
     ta.x = h->x;
@@ -527,6 +564,7 @@ TileArgs tile_args(mp_handle *h) {
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[h->rp ^ 1];
     ta.ctr = h->ctr;
+    ta.tmap = h->d_tmap;
     return ta;
 }
 
@@ -920,6 +958,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->x, dense));
     TRY(cudaMemsetAsync(h->x, 0, dense, h->st));  // x = 0 (solver.py:112)
     TRY(cudaMalloc(&h->snap_x, dense));
+    if ((rc = make_x_tmap(h))) return bail(rc);
     TRY(cudaMalloc(&h->tmp, m * sizeof(double)));
     if ((rc = upload_packed(h, &h->d, inst->d_flat))) return bail(rc);
     if ((rc = upload_packed(h, &h->w, inst->w_flat))) return bail(rc);
