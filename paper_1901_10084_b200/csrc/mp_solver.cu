@@ -528,13 +528,17 @@ typedef CUresult (*encode_tiled_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 int make_x_tmap(mp_handle *h) {
     if (h->kind != 2 || (h->b & 1) || h->b > 256 || getenv("MP_NO_TMA")) return MP_OK;
-    void *fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn) {
+    // resolved once per process (the lookup costs tens of milliseconds)
+    static void *fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
         cudaGetLastError();
-        return MP_OK;  // no encoder: element copies
-    }
+    });
+    if (!fn) return MP_OK;  // no encoder: element copies
     CUtensorMap map;
     // inner extent ld (not n): with an odd n the box loads fault at the row end
     const cuuint64_t dims[2] = {(cuuint64_t)h->ld, (cuuint64_t)h->n};
@@ -547,7 +551,8 @@ int make_x_tmap(mp_handle *h) {
                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     CK(cudaMalloc(&h->d_tmap, sizeof(CUtensorMap)));
-    CK(cudaMemcpy(h->d_tmap, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    // pageable source: the call returns once `map` has been staged
+    CK(cudaMemcpyAsync(h->d_tmap, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
     return MP_OK;
 }
 
