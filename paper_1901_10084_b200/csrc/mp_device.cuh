@@ -119,7 +119,8 @@ struct TileArgs {
     int32_t lw;                 // active lanes per warp slot row (<= 32)
     int32_t colm;               // column-major slot map in each band
     int32_t tl_round;           // MP_TIMELINE builds: round whose first tile is traced
-    const void *tmap;           // 2-D TMA descriptor of x (box b x BLK), null: element copies
+    const void *tmap;           // 2-D TMA descriptor of x (box wkp x BLK), null: element copies
+    int32_t wkp;                // WK row pitch in doubles (>= b; the TMA box width)
 };
 
 #ifdef MP_TIMELINE
@@ -184,6 +185,7 @@ struct CtaConst {
     uint32_t band_mul;    // ceil(2^16 / RB): row -> band ((row * band_mul) >> 16)
     const void *tmap;     // TMA descriptor of x (WK blocks), or null
     int32_t tma_st;       // the tile's K is b wide: interior WK blocks are stored by TMA
+    int32_t wkp;          // WK row pitch (doubles)
 };
 
 // Forwarding of an exact step's x_jk write to the later bands that read it
@@ -730,7 +732,7 @@ __device__ __forceinline__ void wr_finish(WarpDuals *w, const DualPool &p, PassC
 // ilo (stored from row 0 of its WR), and every CTA stages the whole WK; with
 // with_wk = false the WK part is skipped (write-back by the last band only).
 template <int W, bool LOAD>
-__device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld, double *g,
+__device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int64_t ld, double *g,
                                            double *wr, double *wk, int blk, int tid, int nt,
                                            int r0, int r1, bool with_wk) {
 #ifdef MP_EXP_NOWB
@@ -780,7 +782,7 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int64_t ld,
     for (int rr = tid >> 5; rr < BLK; rr += nw) {
         const int j = j0 + rr;
         if (j < jvlo || j > T.jhi) continue;
-        const uint32_t srow = smem_u32(wk + (j & (W - 1)) * b);
+        const uint32_t srow = smem_u32(wk + (j & (W - 1)) * p);
         double *grow = g + (int64_t)j * ld + T.klo;
         for (int kk = lane; kk < b; kk += 32) {
             const int k = T.klo + kk;
@@ -822,10 +824,11 @@ template <int W>
 struct SmemMap {
     int b;
     int rb;  // WR rows staged by this CTA (its band; b without a cluster)
+    int p;   // WK row pitch in doubles (b, or b + 2 against bank conflicts)
     __device__ __host__ int wr() const { return 0; }
     __device__ __host__ int wk() const { return rb * W * 8; }
-    __device__ __host__ int zero() const { return (rb + b) * W * 8; }
-    __device__ __host__ int rk() const { return (rb + b) * W * 8 + W * 8; }
+    __device__ __host__ int zero() const { return rb * W * 8 + p * W * 8; }
+    __device__ __host__ int rk() const { return zero() + W * 8; }
     __device__ __host__ int xbytes() const { return rk() + ((b * b * 8 + W * 8 - 1) / (W * 8)) * W * 8; }
 };
 
@@ -837,7 +840,7 @@ struct SlotGeom {
     int pik[S];       // byte offset of x_ik (RK) or of the zero row
     int wr[S];        // byte offset of WR row ii (or zero row)
     int wk[S];        // byte offset of WK column kk (or zero row)
-    int wkm[S];       // WK row pitch in doubles (b), 0 for an inactive slot
+    int wkm[S];       // WK row pitch in doubles (M.p), 0 for an inactive slot
     int rkr[S];       // RK byte offset of x_ij when j in K:  rkr + 8j
     int rkc[S];       // RK byte offset of x_jk when j in R:  8*b*j + rkc
     int zero;         // shared address of the zero row
@@ -949,7 +952,7 @@ __device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, con
         G.pik[s] = B32 + (ok ? M.rk() + 8 * (ii * b + kk) : M.zero());
         G.wr[s] = B32 + (ok ? M.wr() + (ii - r0) * W * 8 : M.zero());
         G.wk[s] = B32 + (ok ? M.wk() + kk * 8 : M.zero());
-        G.wkm[s] = ok ? b : 0;
+        G.wkm[s] = ok ? M.p : 0;
         G.rkr[s] = B32 + (ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero());
         G.rkc[s] = B32 + (ok ? M.rk() + 8 * (kk - T.ilo * b) : M.zero());
     }
@@ -1028,7 +1031,7 @@ __device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned
 }
 
 #ifndef MP_COLD_INLINE
-#define MP_COLD_INLINE __noinline__
+#define MP_COLD_INLINE __forceinline__  // inlined: no call, registers allocated with the sweep (-2.7% at config 2)
 #endif
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned flagged,
@@ -1399,8 +1402,8 @@ __device__ __forceinline__ void producer_bar(int nthreads) {
 template <int W>
 __device__ __forceinline__ void wk_tma_load(const CtaConst *cc, TileSync *ts, double *WK, int g) {
     unsigned long long *bar = &ts->wkbar[g & (W / BLK - 1)];
-    mbar_expect_tx(bar, (unsigned)(cc->b * BLK * 8));
-    tma_load_2d(smem_u32(WK + ((g * BLK) & (W - 1)) * cc->b), cc->tmap, cc->T.klo, g * BLK, bar);
+    mbar_expect_tx(bar, (unsigned)(cc->wkp * BLK * 8));  // the box is wkp columns wide
+    tma_load_2d(smem_u32(WK + ((g * BLK) & (W - 1)) * cc->wkp), cc->tmap, cc->T.klo, g * BLK, bar);
 }
 template <int W>
 __device__ __forceinline__ void wk_tma_wait(TileSync *ts, int g) {
@@ -1410,7 +1413,7 @@ __device__ __forceinline__ void wk_tma_wait(TileSync *ts, int g) {
 // this tile's x_jk (j > ihi, j >= jlo; rows j >= z hold only k <= j pairs,
 // the unused lower triangle, written back unchanged) and K is b wide.
 __device__ __forceinline__ bool wk_tma_store_ok(const CtaConst *cc, int g) {
-    return cc->tmap != nullptr && cc->tma_st && g * BLK >= max(cc->T.jlo, cc->T.ihi + 1);
+    return cc->tmap != nullptr && cc->tma_st && cc->wkp == cc->b && g * BLK >= max(cc->T.jlo, cc->T.ihi + 1);
 }
 __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1472,10 +1475,10 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
         while (lo_res < low_need) {
             const bool st = last_band && wk_tma_store_ok(cc, lo_res);
-            ring_block<W, false>(T, b, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band && !st);
+            ring_block<W, false>(T, b, cc->wkp, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band && !st);
             if (st && ptid == 0) {
                 fence_proxy_async();  // the compute warps' (acquired) writes, to the async proxy
-                tma_store_2d(cc->tmap, T.klo, lo_res * BLK, smem_u32(WK + ((lo_res * BLK) & (W - 1)) * b));
+                tma_store_2d(cc->tmap, T.klo, lo_res * BLK, smem_u32(WK + ((lo_res * BLK) & (W - 1)) * cc->wkp));
             }
             ++lo_res;
             busy = true;
@@ -1487,14 +1490,14 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         const int want = min(need_fast + LOOKAHEAD, blast);
         while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
             ++hi_issued;
-            ring_block<W, true>(T, b, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, cc->tmap == nullptr);
+            ring_block<W, true>(T, b, cc->wkp, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, cc->tmap == nullptr);
             if (cc->tmap && ptid == 0) {
                 bulk_wait_read_all();  // the slots' previous box store has read them
                 fence_proxy_async();
                 wk_tma_load<W>(cc, ts, WK, hi_issued);
             }
             if (!UNIT)
-                ring_block<W, true>(T, b, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
+                ring_block<W, true>(T, b, cc->wkp, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
                                     WK + xsize, hi_issued, ptid, pn, r0, r1, true);
             cp_async_commit();  // one group per block, same sequence in every thread
             busy = true;
@@ -1574,7 +1577,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const int r0 = band * RB, r1 = min(b, r0 + RB);
     const bool last_band = band == C - 1;
     const int64_t stream_base = T.stream0 + (int64_t)band * nwc;
-    const SmemMap<W> M{b, RB};
+    const SmemMap<W> M{b, RB, a.wkp};
     // TMA boxes need a 16-byte aligned start column: tiles with an odd klo copy
     // WK element by element (the configs' even n give every tile an even klo)
     const void *tmap = (T.klo & 1) ? nullptr : a.tmap;
@@ -1614,6 +1617,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.band_mul = (uint32_t)((65536u + (unsigned)RB - 1) / (unsigned)RB);
         cc.tmap = tmap;
         cc.tma_st = T.z - T.klo + 1 == b;
+        cc.wkp = a.wkp;
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
         cc.B32 = B32;
         cc.lw = a.lw;
@@ -1640,9 +1644,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         for (int bk = lo0; bk <= hi0; ++bk) wk_tma_load<W>(&cc, &ts, WK, bk);
     }
     for (int bk = lo0; bk <= hi0; ++bk) {
-        ring_block<W, true>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, tmap == nullptr);
+        ring_block<W, true>(T, b, a.wkp, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, tmap == nullptr);
         if (!UNIT)
-            ring_block<W, true>(T, b, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
+            ring_block<W, true>(T, b, a.wkp, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
                                 bk, tid, nt, r0, r1, true);
     }
     cp_async_commit();
@@ -1706,10 +1710,10 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     // band holds the final WK (every band forwards its WK writes downstream)
     for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk) {
         const bool st = last_band && wk_tma_store_ok(&cc, bk);
-        ring_block<W, false>(T, b, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band && !st);
+        ring_block<W, false>(T, b, a.wkp, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band && !st);
         if (st && tid == 0) {  // wr_finish (warp 0) waits for the bulk group
             fence_proxy_async();
-            tma_store_2d(tmap, T.klo, bk * BLK, smem_u32(WK + ((bk * BLK) & (W - 1)) * b));
+            tma_store_2d(tmap, T.klo, bk * BLK, smem_u32(WK + ((bk * BLK) & (W - 1)) * a.wkp));
         }
     }
     rk_block<false>(T, b, a.ld, a.x, RK, tid, nt, r0, r1);
@@ -1734,10 +1738,10 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 }
 
 // dynamic shared memory of one CTA
-inline size_t tile_smem_bytes(int b, int W, bool unit, int nt, int rb) {
-    const size_t xb = W == 512   ? SmemMap<512>{b, rb}.xbytes()
-                      : W == 256 ? SmemMap<256>{b, rb}.xbytes()
-                                 : SmemMap<128>{b, rb}.xbytes();
+inline size_t tile_smem_bytes(int b, int W, bool unit, int nt, int rb, int p) {
+    const size_t xb = W == 512   ? SmemMap<512>{b, rb, p}.xbytes()
+                      : W == 256 ? SmemMap<256>{b, rb, p}.xbytes()
+                                 : SmemMap<128>{b, rb, p}.xbytes();
     return (size_t)W * 8 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
 }
 

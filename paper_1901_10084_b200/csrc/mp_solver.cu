@@ -211,6 +211,7 @@ struct mp_handle {
     // tile, S slots per thread, NWC compute + NPW producer warps per CTA
     struct RoundCfg {
         int C = 1, S = 1, NWC = 1, NPW = 1, NT = 64, W = 128, RB = 1, LW = 32;
+        int P = 1;          // WK row pitch in doubles (b, or b + 2: see round_shape)
         bool colm = false;  // column-major slots in each band
         size_t smem = 0;
     };
@@ -227,7 +228,8 @@ struct mp_handle {
     std::vector<int32_t> tile_of_blk; // (iblock, kblock) -> tile index
     int64_t nib = 0, nkb = 0;
     TileDesc *d_tiles = nullptr;
-    void *d_tmap = nullptr;  // 2-D TMA descriptor of x (WK ring blocks), null: element copies
+    void *d_tmap = nullptr;   // 2-D TMA descriptor of x, box b x BLK (WK ring blocks), null: element copies
+    void *d_tmap2 = nullptr;  // the same with box (b + 2) x BLK (padded WK rows)
     int64_t nstreams = 0;
 
     // sparse duals: two pools, pool[rp] holds the previous pass's duals
@@ -277,6 +279,7 @@ struct mp_handle {
         }
         cudaFree(d_tiles);
         cudaFree(d_tmap);
+        cudaFree(d_tmap2);
         cudaFree(d_cubes);
         cudaFree(ctr);
         cudaFree(d_stats);
@@ -413,6 +416,12 @@ int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
     return n;
 }
 
+// WK blocks can move as 2-D TMA boxes (tiled schedule, even b: box rows of
+// b * 8 bytes, a multiple of 16)
+bool tma_possible(const mp_handle *h) {
+    return h->kind == 2 && !(h->b & 1) && h->b + 2 <= 256 && !getenv("MP_NO_TMA");
+}
+
 // Launch shape of a round with C CTAs per tile: the fewest slots per thread S
 // with at most 15 compute warps (any S is correct: a warp waits until its
 // predecessor finished the whole batch), up to 3 producer warps, W = 256
@@ -440,10 +449,19 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
     // ring width: as many j-slots as fit (a cluster's bands drift apart by up
     // to a few hundred levels; the ring bounds that drift)
     c.W = 128;
-    if (h->unit_x && tile_smem_bytes(b, 256, true, c.NT, c.RB) <= 225 * 1024) c.W = 256;
-    if (h->unit_x && C > 1 && S <= 2 && tile_smem_bytes(b, 512, true, c.NT, c.RB) <= 225 * 1024) c.W = 512;
+    if (h->unit_x && tile_smem_bytes(b, 256, true, c.NT, c.RB, b) <= 225 * 1024) c.W = 256;
+    if (h->unit_x && C > 1 && S <= 2 && tile_smem_bytes(b, 512, true, c.NT, c.RB, b) <= 225 * 1024) c.W = 512;
     if (const char *e = getenv("MP_RING_W")) c.W = std::min(c.W, std::max(128, atoi(e)));
-    c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB);
+    // WK row pitch: rows of b doubles map a TMA box one to one, but with b = 8
+    // mod 16 the rows of a column-major band (lanes over i at one k) fall into
+    // two banks; a pitch of b + 2 spreads them over eight.  Padded rows are
+    // loaded as (b + 2)-wide boxes and written back element-wise, so they are
+    // used when they fit beside the chosen ring width (W = 512 bands keep b).
+    c.P = b;
+    if (tma_possible(h) && !getenv("MP_WK_PITCH_B") &&
+        tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB, b + 2) <= 225 * 1024)
+        c.P = b + 2;
+    c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB, c.P);
     return c;
 }
 
@@ -527,7 +545,7 @@ typedef CUresult (*encode_tiled_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32
                                     const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 int make_x_tmap(mp_handle *h) {
-    if (h->kind != 2 || (h->b & 1) || h->b > 256 || getenv("MP_NO_TMA")) return MP_OK;
+    if (!tma_possible(h)) return MP_OK;
     // resolved once per process (the lookup costs tens of milliseconds)
     static void *fn = nullptr;
     static std::once_flag once;
@@ -539,20 +557,23 @@ int make_x_tmap(mp_handle *h) {
         cudaGetLastError();
     });
     if (!fn) return MP_OK;  // no encoder: element copies
-    CUtensorMap map;
-    // inner extent ld (not n): with an odd n the box loads fault at the row end
-    const cuuint64_t dims[2] = {(cuuint64_t)h->ld, (cuuint64_t)h->n};
-    const cuuint64_t strides[1] = {(cuuint64_t)h->ld * sizeof(double)};
-    const cuuint32_t box[2] = {(cuuint32_t)h->b, (cuuint32_t)BLK};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = ((encode_tiled_fn)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->x, dims, strides,
-                                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    CK(cudaMalloc(&h->d_tmap, sizeof(CUtensorMap)));
-    // pageable source: the call returns once `map` has been staged
-    CK(cudaMemcpyAsync(h->d_tmap, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
+    for (int pad = 0; pad <= 2; pad += 2) {
+        CUtensorMap map;
+        // inner extent ld (not n): with an odd n the box loads fault at the row end
+        const cuuint64_t dims[2] = {(cuuint64_t)h->ld, (cuuint64_t)h->n};
+        const cuuint64_t strides[1] = {(cuuint64_t)h->ld * sizeof(double)};
+        const cuuint32_t box[2] = {(cuuint32_t)(h->b + pad), (cuuint32_t)BLK};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = ((encode_tiled_fn)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->x, dims, strides,
+                                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        void *&dst = pad ? h->d_tmap2 : h->d_tmap;
+        CK(cudaMalloc(&dst, sizeof(CUtensorMap)));
+        // pageable source: the call returns once `map` has been staged
+        CK(cudaMemcpyAsync(dst, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
+    }
     return MP_OK;
 }
 
@@ -569,7 +590,6 @@ TileArgs tile_args(mp_handle *h) {
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[h->rp ^ 1];
     ta.ctr = h->ctr;
-    ta.tmap = h->d_tmap;
     return ta;
 }
 
@@ -620,6 +640,8 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     ta.colm = c.colm ? 1 : 0;
     ta.nt = c.NT;
     ta.nwc = c.NWC;
+    ta.wkp = c.P;
+    ta.tmap = c.P == h->b ? h->d_tmap : h->d_tmap2;
     return launch_tiles(h, c, ta, (int)cnt);
 }
 
