@@ -121,6 +121,7 @@ struct TileArgs {
     int32_t tl_round;           // MP_TIMELINE builds: round whose first tile is traced
     const void *tmap;           // 2-D TMA descriptor of x (box wkp x BLK), null: element copies
     int32_t wkp;                // WK row pitch in doubles (>= b; the TMA box width)
+    int32_t wrp;                // WR row pitch in doubles (>= W)
 };
 
 #ifdef MP_TIMELINE
@@ -186,6 +187,7 @@ struct CtaConst {
     const void *tmap;     // TMA descriptor of x (WK blocks), or null
     int32_t tma_st;       // the tile's K is b wide: interior WK blocks are stored by TMA
     int32_t wkp;          // WK row pitch (doubles)
+    int32_t wrp;          // WR row pitch (doubles)
 };
 
 // Forwarding of an exact step's x_jk write to the later bands that read it
@@ -732,7 +734,7 @@ __device__ __forceinline__ void wr_finish(WarpDuals *w, const DualPool &p, PassC
 // ilo (stored from row 0 of its WR), and every CTA stages the whole WK; with
 // with_wk = false the WK part is skipped (write-back by the last band only).
 template <int W, bool LOAD>
-__device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int64_t ld, double *g,
+__device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int pr, int64_t ld, double *g,
                                            double *wr, double *wk, int blk, int tid, int nt,
                                            int r0, int r1, bool with_wk) {
 #ifdef MP_EXP_NOWB
@@ -755,7 +757,7 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int6
             const bool v0 = i <= T.ihi && j >= wlo && j <= whi && i < j;
             const bool v1 = i <= T.ihi && j + 1 >= wlo && j + 1 <= whi && i < j + 1;
             if (!(v0 | v1)) continue;
-            const uint32_t s = smem_u32(wr + ii * W + (j & (W - 1)));
+            const uint32_t s = smem_u32(wr + ii * pr + (j & (W - 1)));
             double *gp = g + (int64_t)i * ld + j;
             if (v0 & v1) {
                 if (LOAD) cp_async16(s, gp);
@@ -784,6 +786,19 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int6
         if (j < jvlo || j > T.jhi) continue;
         const uint32_t srow = smem_u32(wk + (j & (W - 1)) * p);
         double *grow = g + (int64_t)j * ld + T.klo;
+        if (!LOAD && !((T.klo | p) & 1)) {  // write-back in 16-byte pairs (both sides aligned)
+            for (int kk = 2 * lane; kk < b; kk += 64) {
+                const int k = T.klo + kk;
+                const bool v0 = k <= T.z && j < k, v1 = kk + 1 < b && k + 1 <= T.z && j < k + 1;
+                if (v0 & v1) {
+                    st_global_v2(grow + kk, srow + 8 * kk);
+                } else {
+                    if (v0) grow[kk] = ld_sh(srow + 8 * kk);
+                    if (v1) grow[kk + 1] = ld_sh(srow + 8 * kk + 8);
+                }
+            }
+            continue;
+        }
         for (int kk = lane; kk < b; kk += 32) {
             const int k = T.klo + kk;
             if (k <= T.z && j < k) {
@@ -818,18 +833,21 @@ __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, d
 //   [2*b*W*8, +W*8)       ZERO row (dummy target of inactive slots)
 //   then RK[b*b], then (general W) the same layout for 1/reg_x, then the
 //   per-warp dual state.
-// Ring rows are W*8-aligned, so a slot's ring address is one LOP3:
-// ((L - i - k) * 8 & (W*8 - 8)) | row_base.
+// A slot's ring address is ((L - i - k) * 8 & (W*8 - 8)) times the row
+// pitch (WK) or plus the row base (WR); both pitches are padded so that the
+// lanes of a warp spread over the banks (the host picks them per round).
 template <int W>
 struct SmemMap {
     int b;
     int rb;  // WR rows staged by this CTA (its band; b without a cluster)
-    int p;   // WK row pitch in doubles (b, or b + 2 against bank conflicts)
+    int p;   // WK row pitch in doubles (>= b, chosen against bank conflicts)
+    int pr;  // WR row pitch in doubles (>= W, likewise)
+    static __device__ __host__ int up(int x) { return (x + 127) & ~127; }
     __device__ __host__ int wr() const { return 0; }
-    __device__ __host__ int wk() const { return rb * W * 8; }
-    __device__ __host__ int zero() const { return rb * W * 8 + p * W * 8; }
+    __device__ __host__ int wk() const { return up(rb * pr * 8); }
+    __device__ __host__ int zero() const { return wk() + W * p * 8; }
     __device__ __host__ int rk() const { return zero() + W * 8; }
-    __device__ __host__ int xbytes() const { return rk() + ((b * b * 8 + W * 8 - 1) / (W * 8)) * W * 8; }
+    __device__ __host__ int xbytes() const { return up(rk() + b * b * 8); }
 };
 
 template <int S>
@@ -890,13 +908,13 @@ __device__ __forceinline__ void slot_addrs(const SlotGeom<S> &G, int L, int b, i
         if (ALIAS) {
             const bool act = (unsigned)(L - G.off[s]) <= G.span[s];
             const int j = j8 >> 3;
-            int a0 = j >= klo ? G.rkr[s] + j8 : (jm | G.wr[s]);
+            int a0 = j >= klo ? G.rkr[s] + j8 : jm + G.wr[s];
             int e0 = j <= ihi ? j * (8 * b) + G.rkc[s] : jm * G.wkm[s] + G.wk[s];
             pa[s] = act ? a0 : G.zero;
             pe[s] = act ? e0 : G.zero;
             pc[s] = act ? G.pik[s] : G.zero;
         } else {
-            pa[s] = jm | G.wr[s];
+            pa[s] = jm + G.wr[s];
             pe[s] = jm * G.wkm[s] + G.wk[s];
             pc[s] = G.pik[s];
         }
@@ -950,7 +968,7 @@ __device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, con
         G.off[s] = ok ? i + k + js : 0x3fffffff;
         G.span[s] = ok ? (unsigned)(je - js) : 0u;
         G.pik[s] = B32 + (ok ? M.rk() + 8 * (ii * b + kk) : M.zero());
-        G.wr[s] = B32 + (ok ? M.wr() + (ii - r0) * W * 8 : M.zero());
+        G.wr[s] = B32 + (ok ? M.wr() + (ii - r0) * M.pr * 8 : M.zero());
         G.wk[s] = B32 + (ok ? M.wk() + kk * 8 : M.zero());
         G.wkm[s] = ok ? M.p : 0;
         G.rkr[s] = B32 + (ok ? M.rk() + 8 * (ii * b - T.klo) : M.zero());
@@ -1429,7 +1447,7 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
     const int C = cc->C, band = cc->band;
     const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
     const bool last_band = band == C - 1;
-    double *WR = smd, *WK = smd + cc->RB * W;
+    double *WR = smd, *WK = smd + SmemMap<W>{b, cc->RB, cc->wkp, cc->wrp}.wk() / 8;
     const int xsize = cc->xsize;
     const int blast = T.jhi / BLK;
     const uint32_t band0_done = C > 1 ? mapa(smem_u32(&ts->done[0]), 0) : 0u;
@@ -1475,7 +1493,7 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
         while (lo_res < low_need) {
             const bool st = last_band && wk_tma_store_ok(cc, lo_res);
-            ring_block<W, false>(T, b, cc->wkp, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band && !st);
+            ring_block<W, false>(T, b, cc->wkp, cc->wrp, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band && !st);
             if (st && ptid == 0) {
                 fence_proxy_async();  // the compute warps' (acquired) writes, to the async proxy
                 tma_store_2d(cc->tmap, T.klo, lo_res * BLK, smem_u32(WK + ((lo_res * BLK) & (W - 1)) * cc->wkp));
@@ -1490,14 +1508,14 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
         const int want = min(need_fast + LOOKAHEAD, blast);
         while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
             ++hi_issued;
-            ring_block<W, true>(T, b, cc->wkp, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, cc->tmap == nullptr);
+            ring_block<W, true>(T, b, cc->wkp, cc->wrp, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, cc->tmap == nullptr);
             if (cc->tmap && ptid == 0) {
                 bulk_wait_read_all();  // the slots' previous box store has read them
                 fence_proxy_async();
                 wk_tma_load<W>(cc, ts, WK, hi_issued);
             }
             if (!UNIT)
-                ring_block<W, true>(T, b, cc->wkp, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
+                ring_block<W, true>(T, b, cc->wkp, cc->wrp, cc->ld, const_cast<double *>(cc->winvx), WR + xsize,
                                     WK + xsize, hi_issued, ptid, pn, r0, r1, true);
             cp_async_commit();  // one group per block, same sequence in every thread
             busy = true;
@@ -1577,13 +1595,13 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const int r0 = band * RB, r1 = min(b, r0 + RB);
     const bool last_band = band == C - 1;
     const int64_t stream_base = T.stream0 + (int64_t)band * nwc;
-    const SmemMap<W> M{b, RB, a.wkp};
+    const SmemMap<W> M{b, RB, a.wkp, a.wrp};
     // TMA boxes need a 16-byte aligned start column: tiles with an odd klo copy
     // WK element by element (the configs' even n give every tile an even klo)
     const void *tmap = (T.klo & 1) ? nullptr : a.tmap;
     // base aligned to W*8 bytes (the launch reserves the slack) so ring rows
     // are W*8-aligned shared addresses and a slot address is one LOP3
-    unsigned char *sm = smem_raw + ((W * 8 - (smem_u32(smem_raw) & (W * 8 - 1))) & (W * 8 - 1));
+    unsigned char *sm = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int B32 = (int)smem_u32(sm);
     double *smd = reinterpret_cast<double *>(sm);
     const int xb = M.xbytes();
@@ -1618,6 +1636,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.tmap = tmap;
         cc.tma_st = T.z - T.klo + 1 == b;
         cc.wkp = a.wkp;
+        cc.wrp = a.wrp;
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
         cc.B32 = B32;
         cc.lw = a.lw;
@@ -1644,9 +1663,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         for (int bk = lo0; bk <= hi0; ++bk) wk_tma_load<W>(&cc, &ts, WK, bk);
     }
     for (int bk = lo0; bk <= hi0; ++bk) {
-        ring_block<W, true>(T, b, a.wkp, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, tmap == nullptr);
+        ring_block<W, true>(T, b, a.wkp, a.wrp, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, tmap == nullptr);
         if (!UNIT)
-            ring_block<W, true>(T, b, a.wkp, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
+            ring_block<W, true>(T, b, a.wkp, a.wrp, a.ld, const_cast<double *>(a.winvx), WR + xsize, WK + xsize,
                                 bk, tid, nt, r0, r1, true);
     }
     cp_async_commit();
@@ -1710,7 +1729,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     // band holds the final WK (every band forwards its WK writes downstream)
     for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk) {
         const bool st = last_band && wk_tma_store_ok(&cc, bk);
-        ring_block<W, false>(T, b, a.wkp, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band && !st);
+        ring_block<W, false>(T, b, a.wkp, a.wrp, a.ld, a.x, WR, WK, bk, tid, nt, r0, r1, last_band && !st);
         if (st && tid == 0) {  // wr_finish (warp 0) waits for the bulk group
             fence_proxy_async();
             tma_store_2d(tmap, T.klo, bk * BLK, smem_u32(WK + ((bk * BLK) & (W - 1)) * a.wkp));
@@ -1738,11 +1757,12 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 }
 
 // dynamic shared memory of one CTA
-inline size_t tile_smem_bytes(int b, int W, bool unit, int nt, int rb, int p) {
-    const size_t xb = W == 512   ? SmemMap<512>{b, rb, p}.xbytes()
-                      : W == 256 ? SmemMap<256>{b, rb, p}.xbytes()
-                                 : SmemMap<128>{b, rb, p}.xbytes();
-    return (size_t)W * 8 + xb * (unit ? 1 : 2) + (size_t)(nt / 32) * sizeof(WarpDuals);
+inline size_t tile_smem_bytes(int b, int W, bool unit, int nwc, int rb, int p, int pr) {
+    const size_t xb = W == 512   ? SmemMap<512>{b, rb, p, pr}.xbytes()
+                      : W == 256 ? SmemMap<256>{b, rb, p, pr}.xbytes()
+                                 : SmemMap<128>{b, rb, p, pr}.xbytes();
+    // 128 bytes of alignment slack; dual-stream state for the compute warps only
+    return 128 + xb * (unit ? 1 : 2) + (size_t)nwc * sizeof(WarpDuals);
 }
 
 }  // namespace mp

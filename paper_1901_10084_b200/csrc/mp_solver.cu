@@ -211,7 +211,8 @@ struct mp_handle {
     // tile, S slots per thread, NWC compute + NPW producer warps per CTA
     struct RoundCfg {
         int C = 1, S = 1, NWC = 1, NPW = 1, NT = 64, W = 128, RB = 1, LW = 32;
-        int P = 1;          // WK row pitch in doubles (b, or b + 2: see round_shape)
+        int P = 1;          // WK row pitch in doubles (>= b: see round_shape)
+        int PR = 128;       // WR row pitch in doubles (>= W)
         bool colm = false;  // column-major slots in each band
         size_t smem = 0;
     };
@@ -228,8 +229,9 @@ struct mp_handle {
     std::vector<int32_t> tile_of_blk; // (iblock, kblock) -> tile index
     int64_t nib = 0, nkb = 0;
     TileDesc *d_tiles = nullptr;
-    void *d_tmap = nullptr;   // 2-D TMA descriptor of x, box b x BLK (WK ring blocks), null: element copies
-    void *d_tmap2 = nullptr;  // the same with box (b + 2) x BLK (padded WK rows)
+    // 2-D TMA descriptors of x with box (b + 2t) x BLK, t = 0..7 (WK ring blocks
+    // of row pitch b + 2t); null: element copies
+    void *d_tmap[8] = {};
     int64_t nstreams = 0;
 
     // sparse duals: two pools, pool[rp] holds the previous pass's duals
@@ -278,8 +280,7 @@ struct mp_handle {
             cudaFree(p.head);
         }
         cudaFree(d_tiles);
-        cudaFree(d_tmap);
-        cudaFree(d_tmap2);
+        for (void *t : d_tmap) cudaFree(t);
         cudaFree(d_cubes);
         cudaFree(ctr);
         cudaFree(d_stats);
@@ -422,6 +423,45 @@ bool tma_possible(const mp_handle *h) {
     return h->kind == 2 && !(h->b & 1) && h->b + 2 <= 256 && !getenv("MP_NO_TMA");
 }
 
+// Shared-memory wavefronts per warp-wide 8-byte ring load (x_ij from WR
+// with row pitch `pitch`, or x_jk from WK with row pitch `pitch`), averaged
+// over the round's compute warps, slots and 16 consecutive levels: per
+// half-warp, the most distinct addresses that share one of the 16 8-byte
+// bank pairs.
+double ring_waves(const mp_handle::RoundCfg &c, int b, int pitch, bool wk) {
+    double tot = 0.0;
+    int n = 0;
+    for (int w = 0; w < c.NWC; ++w)
+        for (int s = 0; s < c.S; ++s)
+            for (int L = 0; L < 16; ++L) {
+                for (int half = 0; half < 2; ++half) {
+                    int64_t addr[16];
+                    int na = 0;
+                    for (int ln = 16 * half; ln < 16 * half + 16; ++ln) {
+                        const int q = (w * c.S + s) * c.LW + ln;
+                        if (ln >= c.LW || q >= c.RB * b) continue;
+                        const int ii = c.colm ? q % c.RB : q / b, kk = c.colm ? q / c.RB : q % b;
+                        const int jm = (4096 + L - ii - kk) & (c.W - 1);
+                        addr[na++] = wk ? (int64_t)jm * pitch + kk : (int64_t)ii * pitch + jm;
+                    }
+                    int worst = 0;
+                    for (int bank = 0; bank < 16; ++bank) {
+                        int cnt = 0;
+                        for (int x = 0; x < na; ++x) {
+                            if ((addr[x] & 15) != bank) continue;
+                            bool dup = false;
+                            for (int y = 0; y < x; ++y) dup |= addr[y] == addr[x];
+                            cnt += !dup;
+                        }
+                        worst = std::max(worst, cnt);
+                    }
+                    tot += worst;
+                }
+                ++n;
+            }
+    return n ? tot / n : 0.0;
+}
+
 // Launch shape of a round with C CTAs per tile: the fewest slots per thread S
 // with at most 15 compute warps (any S is correct: a warp waits until its
 // predecessor finished the whole batch), up to 3 producer warps, W = 256
@@ -448,20 +488,44 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
     c.NT = 32 * (c.NWC + c.NPW);
     // ring width: as many j-slots as fit (a cluster's bands drift apart by up
     // to a few hundred levels; the ring bounds that drift)
+    auto fits = [&](int W, int P, int PR) {
+        return tile_smem_bytes(b, W, h->unit_x, c.NWC, c.RB, P, PR) <= 225 * 1024;
+    };
     c.W = 128;
-    if (h->unit_x && tile_smem_bytes(b, 256, true, c.NT, c.RB, b) <= 225 * 1024) c.W = 256;
-    if (h->unit_x && C > 1 && S <= 2 && tile_smem_bytes(b, 512, true, c.NT, c.RB, b) <= 225 * 1024) c.W = 512;
+    if (h->unit_x && fits(256, b, 256)) c.W = 256;
+    if (h->unit_x && C > 1 && S <= 2 && fits(512, b, 512)) c.W = 512;
     if (const char *e = getenv("MP_RING_W")) c.W = std::min(c.W, std::max(128, atoi(e)));
-    // WK row pitch: rows of b doubles map a TMA box one to one, but with b = 8
-    // mod 16 the rows of a column-major band (lanes over i at one k) fall into
-    // two banks; a pitch of b + 2 spreads them over eight.  Padded rows are
-    // loaded as (b + 2)-wide boxes and written back element-wise, so they are
-    // used when they fit beside the chosen ring width (W = 512 bands keep b).
+    // Row pitches against bank conflicts: the lanes of a warp read x_ij at
+    // WR[i][j % W] and x_jk at WK[j % W][k] with j = L - i - k, so with the
+    // plain pitches (W, b) lanes with equal i + k (or equal i mod 2 when b =
+    // 8 mod 16) share a bank.  Pick the pitches with the fewest shared-memory
+    // wavefronts for this round's lane map (even pitches keep 16-byte pairs
+    // aligned; a WK pitch > b is loaded as a wider TMA box and written back
+    // element-wise).
+    c.PR = c.W;
+    if (!getenv("MP_WR_PITCH_W")) {
+        double best = 1e30;
+        for (int pr = c.W; pr <= c.W + 14; pr += 2) {
+            const double v = ring_waves(c, b, pr, false);
+            if (v < best - 1e-9 && fits(c.W, b, pr)) best = v, c.PR = pr;
+        }
+    }
     c.P = b;
-    if (tma_possible(h) && !getenv("MP_WK_PITCH_B") &&
-        tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB, b + 2) <= 225 * 1024)
-        c.P = b + 2;
-    c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NT, c.RB, c.P);
+    if (!getenv("MP_WK_PITCH_B")) {
+        const int step = (b & 1) ? 1 : 2;
+        const double plain = ring_waves(c, b, b, true);
+        double best = 1e30;
+        int bestp = b;
+        for (int pk = b; pk <= b + 14 && pk <= 256; pk += step) {
+            const double v = ring_waves(c, b, pk, true);
+            if (v < best - 1e-9 && fits(c.W, pk, c.PR)) best = v, bestp = pk;
+        }
+        // a padded WK loses the box write-back of the last band: worth it only
+        // when it at least halves the wavefronts (measured: RB = 5 at b = 40,
+        // 5.6 -> 3.3 wavefronts, is a wash; RB >= 8, 8 -> 2, is not)
+        if (best * 2.0 <= plain) c.P = bestp;
+    }
+    c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NWC, c.RB, c.P, c.PR);
     return c;
 }
 
@@ -504,8 +568,8 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         for (int C = 1; C <= 8; ++C)
             if (hist[(size_t)C]) {
                 const mp_handle::RoundCfg c = round_shape(h, C);
-                fprintf(stderr, " C=%d:%d (S=%d NWC=%d NT=%d smem=%zu cap=%d)", C, hist[(size_t)C], c.S,
-                        c.NWC, c.NT, c.smem, C > 1 ? cap[(size_t)C] : -1);
+                fprintf(stderr, " C=%d:%d (S=%d NWC=%d NT=%d W=%d P=%d PR=%d smem=%zu cap=%d)", C, hist[(size_t)C],
+                        c.S, c.NWC, c.NT, c.W, c.P, c.PR, c.smem, C > 1 ? cap[(size_t)C] : -1);
             }
         fprintf(stderr, "\n");
     }
@@ -557,7 +621,8 @@ int make_x_tmap(mp_handle *h) {
         cudaGetLastError();
     });
     if (!fn) return MP_OK;  // no encoder: element copies
-    for (int pad = 0; pad <= 2; pad += 2) {
+    for (int t = 0; t < 8 && h->b + 2 * t <= 256; ++t) {
+        const int pad = 2 * t;
         CUtensorMap map;
         // inner extent ld (not n): with an odd n the box loads fault at the row end
         const cuuint64_t dims[2] = {(cuuint64_t)h->ld, (cuuint64_t)h->n};
@@ -569,12 +634,18 @@ int make_x_tmap(mp_handle *h) {
                                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-        void *&dst = pad ? h->d_tmap2 : h->d_tmap;
+        void *&dst = h->d_tmap[t];
         CK(cudaMalloc(&dst, sizeof(CUtensorMap)));
         // pageable source: the call returns once `map` has been staged
         CK(cudaMemcpyAsync(dst, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice, h->st));
     }
     return MP_OK;
+}
+
+// descriptor for WK row pitch p (box p x BLK), or null
+const void *x_tmap(const mp_handle *h, int p) {
+    const int t = (p - h->b) / 2;
+    return (p - h->b) % 2 == 0 && t >= 0 && t < 8 ? h->d_tmap[t] : nullptr;
 }
 
 TileArgs tile_args(mp_handle *h) {
@@ -641,7 +712,8 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     ta.nt = c.NT;
     ta.nwc = c.NWC;
     ta.wkp = c.P;
-    ta.tmap = c.P == h->b ? h->d_tmap : h->d_tmap2;
+    ta.wrp = c.PR;
+    ta.tmap = x_tmap(h, c.P);
     return launch_tiles(h, c, ta, (int)cnt);
 }
 
