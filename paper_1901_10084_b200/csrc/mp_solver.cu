@@ -431,9 +431,9 @@ bool tma_possible(const mp_handle *h) {
 double ring_waves(const mp_handle::RoundCfg &c, int b, int pitch, bool wk) {
     double tot = 0.0;
     int n = 0;
-    for (int w = 0; w < c.NWC; ++w)
+    for (int w = 0; w < std::min(c.NWC, 4); ++w)  // the lane map repeats with a shift
         for (int s = 0; s < c.S; ++s)
-            for (int L = 0; L < 16; ++L) {
+            for (int L = 0; L < 8; ++L) {
                 for (int half = 0; half < 2; ++half) {
                     int64_t addr[16];
                     int na = 0;
@@ -442,19 +442,13 @@ double ring_waves(const mp_handle::RoundCfg &c, int b, int pitch, bool wk) {
                         if (ln >= c.LW || q >= c.RB * b) continue;
                         const int ii = c.colm ? q % c.RB : q / b, kk = c.colm ? q / c.RB : q % b;
                         const int jm = (4096 + L - ii - kk) & (c.W - 1);
-                        addr[na++] = wk ? (int64_t)jm * pitch + kk : (int64_t)ii * pitch + jm;
+                        const int64_t a = wk ? (int64_t)jm * pitch + kk : (int64_t)ii * pitch + jm;
+                        bool dup = false;  // one address read by several lanes is a broadcast
+                        for (int y = 0; y < na; ++y) dup |= addr[y] == a;
+                        if (!dup) addr[na++] = a;
                     }
-                    int worst = 0;
-                    for (int bank = 0; bank < 16; ++bank) {
-                        int cnt = 0;
-                        for (int x = 0; x < na; ++x) {
-                            if ((addr[x] & 15) != bank) continue;
-                            bool dup = false;
-                            for (int y = 0; y < x; ++y) dup |= addr[y] == addr[x];
-                            cnt += !dup;
-                        }
-                        worst = std::max(worst, cnt);
-                    }
+                    int cnt[16] = {}, worst = 0;
+                    for (int x = 0; x < na; ++x) worst = std::max(worst, ++cnt[addr[x] & 15]);
                     tot += worst;
                 }
                 ++n;
@@ -544,6 +538,8 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     int cmax = 8;
     if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(8, atoi(e)));
     std::vector<int> cap(9, -1);  // co-resident clusters per C (queried once)
+    std::vector<mp_handle::RoundCfg> shape(9);  // launch shape per C (computed once)
+    std::vector<bool> have(9, false);
     h->rcfg.clear();
     for (size_t r = 0; r < cnt_r.size(); ++r) {
         const int64_t cnt = cnt_r[r];
@@ -551,7 +547,8 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         for (int C = std::min(cmax, b); C >= 2 && cnt > 0; --C) {
             const int RB = (b + C - 1) / C;
             if ((C - 1) * RB >= b || cnt * C > sms) continue;
-            const mp_handle::RoundCfg c = round_shape(h, C);
+            if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
+            const mp_handle::RoundCfg &c = shape[C];
             if (c.S > MAX_SLOTS || c.smem > 227 * 1024) continue;
             if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
             if (cap[C] >= cnt) {

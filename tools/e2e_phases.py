@@ -36,3 +36,11 @@ st = s.run(23)
 t1 = _t.perf_counter()
 print(f"run(23) in one call: {1e3*(t1-t0):.1f} ms  device sum {sum(x.wall_time for x in st)*1e3:.1f} ms")
 s.close()
+if os.environ.get("PROFILE"):
+    import cProfile
+    import pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    solve(inst, SolverConfig(tile_size=40, fixed_passes=23))
+    pr.disable()
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
