@@ -1193,10 +1193,18 @@ struct TileSync {
 // copy of it has landed.
 // (Other bands' entries are back-pressure only -- this warp never reads their
 // rings -- so relaxed loads do; the own band's ring data is acquired.)
+// The other bands' entries are this CTA's own copies, stored remotely by
+// their producers: a volatile shared load (LDS) sees them; a stale value only
+// delays (entries grow monotonically), so no cluster-scope load is needed.
+__device__ __forceinline__ int ld_volatile_sh(const int *p) {
+    int v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
 __device__ __forceinline__ int landed_min(TileSync &ts, int C, int band) {
     int m = ld_acquire(&ts.landed_by[band]);
     for (int d = 0; d < C; ++d)
-        if (d != band) m = min(m, ld_relaxed_cluster(smem_u32(&ts.landed_by[d])));
+        if (d != band) m = min(m, ld_volatile_sh(&ts.landed_by[d]));
     return m;
 }
 
@@ -1231,7 +1239,7 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
 }
 
 #ifndef MP_BATCH
-#define MP_BATCH 6
+#define MP_BATCH 8
 #endif
 
 // Sweep levels [La, Lb] of one phase.  Levels are taken in batches of U: in
