@@ -261,3 +261,29 @@ def test_dual_pool_overflow_rolls_back(oracle_lib, monkeypatch, kind, cluster):
     o1, o2 = np.argsort(keys), np.argsort(rk)
     assert np.array_equal(keys[o1], rk[o2]) and np.array_equal(vals[o1], rv[o2])
     sess.close()
+
+
+@pytest.mark.parametrize("n", [180, 181])  # even n: TMA boxes for WK; odd n: odd klo, element copies
+@pytest.mark.parametrize("cluster", [8, 4, 1])
+@pytest.mark.parametrize("env", [{}, {"MP_WR_PITCH_W": "1", "MP_WK_PITCH_B": "1"}, {"MP_NO_TMA": "1"}])
+def test_ring_staging_variants_bitwise(oracle_lib, monkeypatch, n, cluster, env):
+    """Every way of staging the j-rings -- WK as 2-D TMA boxes (plain or
+    padded row pitch, box or 16-byte write-back) or element by element,
+    padded or plain WR pitch -- gives the reference trajectory bit for bit."""
+    monkeypatch.setenv("MP_CLUSTER", str(cluster))
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inst = instances.config_instance(2, n=n)
+    sess = DeviceSession(inst, "tiled", 40)
+    ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=40, workers=4)
+    for _ in range(4):
+        st = sess.run(1)[0]
+        rs = ref.run_pass()
+        assert st.max_violation == rs.max_violation
+    x, f = sess.state()
+    assert np.array_equal(x, ref.state()[0]) and np.array_equal(f, ref.state()[1])
+    keys, vals, _ = sess.duals()
+    rk, rv = ref.duals()
+    o1, o2 = np.argsort(keys), np.argsort(rk)
+    assert np.array_equal(keys[o1], rk[o2]) and np.array_equal(vals[o1], rv[o2])
+    sess.close()
