@@ -229,6 +229,14 @@ __global__ void scan_pair_kernel(const double *x, int64_t ld, const double *f, c
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, viol);
 }
 
+// Dykstra start f = (-w) / (eps * reg_f) (solver.py:108-113), the reference's
+// association and IEEE division (reg_f null: W = I, eps * 1.0 = eps exactly)
+__global__ void f_init_kernel(const double *w, const double *regf, double eps, double *f, int64_t m) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x)
+        f[p] = __ddiv_rn(-w[p], __dmul_rn(eps, regf ? regf[p] : 1.0));
+}
+
 __global__ void reciprocal_kernel(const double *in, double *out, int64_t m) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
          p += (int64_t)gridDim.x * blockDim.x)

@@ -15,11 +15,14 @@
 #include <nccl.h>  // types only: the functions are resolved at run time (nccl_api)
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -45,6 +48,134 @@ int fail(int code, const char *fmt, ...) {
     g_err = buf;
     return code;
 }
+
+// Device buffers of a finished session are kept for the next session of the
+// same shape (repeated solve() calls: cudaMalloc/cudaFree of ~20 buffers cost
+// milliseconds per session).  Only the handle destructor returns buffers,
+// after synchronizing the session's stream; buffers are matched by exact size
+// and device; at most 8 GiB are kept per process, and the cache is emptied
+// and the allocation retried when cudaMalloc runs out of memory.
+struct DevCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void *> free_;
+    std::map<void *, std::pair<int, size_t>> size_;
+    size_t bytes = 0;
+};
+DevCache &dev_cache() {
+    static DevCache *c = new DevCache();  // never destroyed: no frees after the driver unloads
+    return *c;
+}
+cudaError_t dev_malloc(void **p, size_t sz) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    DevCache &c = dev_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.free_.find({dev, sz});
+        if (it != c.free_.end()) {
+            *p = it->second;
+            c.free_.erase(it);
+            c.bytes -= sz;
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(p, sz);
+    if (e == cudaErrorMemoryAllocation) {  // drop the cache and retry
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto &kv : c.free_) {
+            c.size_.erase(kv.second);
+            cudaFree(kv.second);
+        }
+        c.free_.clear();
+        c.bytes = 0;
+        e = cudaMalloc(p, sz);
+    }
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.size_[*p] = {dev, sz};
+    }
+    return e;
+}
+// return a buffer to the cache (the caller has synchronized its users)
+void dev_release(void *p) {
+    if (!p) return;
+    DevCache &c = dev_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.size_.find(p);
+    if (it == c.size_.end() || c.bytes + it->second.second > (size_t(8) << 30)) {
+        if (it != c.size_.end()) c.size_.erase(it);
+        cudaFree(p);
+        return;
+    }
+    c.free_.insert({it->second, p});
+    c.bytes += it->second.second;
+}
+// a buffer freed outside the destructor (pool growth) is really freed
+cudaError_t dev_free(void *p) {
+    if (!p) return cudaSuccess;
+    DevCache &c = dev_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.size_.erase(p);
+    }
+    return cudaFree(p);
+}
+// Small pinned blocks (per-session stats) are recycled the same way.
+std::mutex g_pin_mu;
+std::vector<void *> g_pin_free;
+constexpr size_t PIN_BLOCK = 256;
+cudaError_t pin_malloc(void **p, size_t sz) {
+    if (sz <= PIN_BLOCK) {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        if (!g_pin_free.empty()) {
+            *p = g_pin_free.back();
+            g_pin_free.pop_back();
+            return cudaSuccess;
+        }
+    }
+    return cudaMallocHost(p, std::max(sz, PIN_BLOCK));
+}
+void pin_release(void *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_free.size() < 256) g_pin_free.push_back(p);
+    else cudaFreeHost(p);
+}
+// Pinned staging for the large device -> host reads (dual pools, pair duals):
+// one process-wide buffer, grown on demand, held under its mutex while used.
+struct PinnedStage {
+    std::mutex mu;
+    void *p = nullptr;
+    size_t cap = 0;
+    void *get(size_t sz) {  // caller holds mu
+        if (sz > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            if (cudaMallocHost(&p, sz) != cudaSuccess) {
+                cudaGetLastError();
+                p = nullptr;
+                return nullptr;
+            }
+            cap = sz;
+        }
+        return p;
+    }
+};
+PinnedStage &pinned_stage() {
+    static PinnedStage *s = new PinnedStage();
+    return *s;
+}
+// Dual-pool capacity a previous session of the same shape grew to: the next
+// one starts there (no re-allocation during its first passes, and its pool
+// buffers come back from the cache).
+std::mutex g_hint_mu;
+std::map<std::tuple<int64_t, int, int, int64_t>, int32_t> g_pool_hint;
+}  // namespace
+#define cudaMalloc(p, sz) dev_malloc(reinterpret_cast<void **>(p), (sz))
+#define cudaFree(p) dev_free(reinterpret_cast<void *>(p))
+namespace {
 
 #define NCK(call)                                                                     \
     do {                                                                              \
@@ -271,23 +402,23 @@ struct mp_handle {
 
     ~mp_handle() {
         if (dev >= 0) cudaSetDevice(dev);
+        if (st) cudaStreamSynchronize(st);  // nothing in flight uses the buffers below
         double *bufs[] = {x, winvx, f, d, w, regx, regf, winvf, pu, pl, tmp,
                           snap_x, snap_f, snap_pu, snap_pl, partials};
-        for (double *p : bufs)
-            if (p) cudaFree(p);
+        for (double *p : bufs) dev_release(p);
         for (auto &p : pool) {
-            cudaFree(p.rec);
-            cudaFree(p.head);
+            dev_release(p.rec);
+            dev_release(p.head);
         }
-        cudaFree(d_tiles);
-        for (void *t : d_tmap) cudaFree(t);
-        cudaFree(d_cubes);
-        cudaFree(ctr);
-        cudaFree(d_stats);
-        cudaFree(d_scan);
-        cudaFree(trace);
-        cudaFree(flush);
-        if (h_stats) cudaFreeHost(h_stats);
+        dev_release(d_tiles);
+        for (void *t : d_tmap) dev_release(t);
+        dev_release(d_cubes);
+        dev_release(ctr);
+        dev_release(d_stats);
+        dev_release(d_scan);
+        dev_release(trace);
+        dev_release(flush);
+        pin_release(h_stats);
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
         cudaFree(sh.d_my_tiles);
@@ -304,6 +435,11 @@ struct mp_handle {
 namespace {
 
 int alloc_pool(mp_handle *h, int which, int32_t cap) {
+    {
+        std::lock_guard<std::mutex> lk(g_hint_mu);
+        int32_t &hint = g_pool_hint[{h->n, h->b, h->kind, h->nstreams}];
+        hint = std::max(hint, cap);
+    }
     DualPool &p = h->pool[which];
     cudaFree(p.rec);
     p.rec = nullptr;
@@ -905,6 +1041,20 @@ const char *mp_version(void) { return "metricproj_b200 0.1.0 (sm_100a)"; }
 
 int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     g_err.clear();
+    // MP_TIME_CREATE: wall time of the creation phases on stderr
+    const bool tcr = getenv("MP_TIME_CREATE") != nullptr;
+    cudaStream_t tst = nullptr;
+    auto tnow = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    double tc0 = tcr ? tnow() : 0.0;
+    auto tmark = [&](const char *what) {
+        if (!tcr) return;
+        if (tst) cudaStreamSynchronize(tst);
+        const double t = tnow();
+        fprintf(stderr, "[mp] create %-14s %7.3f ms\n", what, t - tc0);
+        tc0 = t;
+    };
     if (!inst || !cfg || !out) return fail(MP_ERR_ARG, "null argument");
     *out = nullptr;
     const int64_t n = inst->n;
@@ -929,11 +1079,12 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
                     cudaGetErrorString(e));
     if (cfg->device < 0 || cfg->device >= ndev)
         return fail(MP_ERR_ARG, "device %d out of range (%d devices)", cfg->device, ndev);
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, cfg->device));
-    if (prop.major != 10)
+    int cc_major = 0, cc_minor = 0;  // (cudaGetDeviceProperties costs milliseconds)
+    CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, cfg->device));
+    CK(cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, cfg->device));
+    if (cc_major != 10)
         return fail(MP_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", cfg->device,
-                    prop.major, prop.minor);
+                    cc_major, cc_minor);
 
     mp_handle *h = new mp_handle();
     h->dev = cfg->device;
@@ -944,6 +1095,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     if (cudaSetDevice(h->dev) != cudaSuccess) return bail(fail(MP_ERR_CUDA, "cudaSetDevice"));
     if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(MP_ERR_CUDA, "stream create"));
+    tst = h->st;
+    tmark("device+stream");
     h->n = n;
     h->m = pair_count(n);
     h->ld = (n + 31) / 32 * 32;
@@ -1030,6 +1183,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         h->nstreams = (int64_t)h->cubes.size() * CUBE_WARPS;
     }
 
+    tmark("schedule");
     int rc;
 #define TRY(call)                        \
     do {                                 \
@@ -1055,6 +1209,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMemsetAsync(h->x, 0, dense, h->st));  // x = 0 (solver.py:112)
     TRY(cudaMalloc(&h->snap_x, dense));
     if ((rc = make_x_tmap(h))) return bail(rc);
+    tmark("x+tmap");
     TRY(cudaMalloc(&h->tmp, m * sizeof(double)));
     if ((rc = upload_packed(h, &h->d, inst->d_flat))) return bail(rc);
     if ((rc = upload_packed(h, &h->w, inst->w_flat))) return bail(rc);
@@ -1073,13 +1228,11 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         TRY(cudaGetLastError());
     }
     // f = -w / (eps * reg_f)  (solver.py:112), computed as numpy does
-    {
-        std::vector<double> f0((size_t)m);
-        for (int64_t p = 0; p < m; ++p)
-            f0[(size_t)p] = (-inst->w_flat[p]) / (inst->epsilon * (inst->reg_f ? inst->reg_f[p] : 1.0));
-        if ((rc = upload_packed(h, &h->f, f0.data()))) return bail(rc);
-        TRY(cudaStreamSynchronize(h->st));
-    }
+    // f = -w / (eps * reg_f) (solver.py:108-113), IEEE division on the device
+    TRY(cudaMalloc(&h->f, m * sizeof(double)));
+    f_init_kernel<<<egrid, 256, 0, h->st>>>(h->w, h->unit_f ? nullptr : h->regf, h->eps, h->f, m);
+    TRY(cudaGetLastError());
+    tmark("upload d,w,f");
     TRY(cudaMalloc(&h->pu, m * sizeof(double)));
     TRY(cudaMalloc(&h->pl, m * sizeof(double)));
     TRY(cudaMemsetAsync(h->pu, 0, m * sizeof(double), h->st));
@@ -1092,6 +1245,11 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     // about one chunk per stream: the first pass writes into most streams
     int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams + h->nstreams / 4), 1 << 22);
     if (const char *e = getenv("MP_POOL_CAP0")) cap0 = std::max(1, atoi(e));  // tests: force overflow
+    if (!getenv("MP_POOL_CAP0")) {
+        std::lock_guard<std::mutex> lk(g_hint_mu);
+        auto it = g_pool_hint.find({n, b, h->kind, h->nstreams});
+        if (it != g_pool_hint.end()) cap0 = std::max(cap0, it->second);
+    }
     if ((rc = alloc_pool(h, 0, cap0))) return bail(rc);
     if ((rc = alloc_pool(h, 1, cap0))) return bail(rc);
     h->pair_grid = grid_for(m, 256, 148 * 8);
@@ -1099,9 +1257,10 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->ctr, sizeof(PassCounters)));
     TRY(cudaMalloc(&h->d_stats, sizeof(DevStats)));
     TRY(cudaMalloc(&h->d_scan, sizeof(unsigned long long)));
-    TRY(cudaMallocHost(&h->h_stats, sizeof(DevStats)));
+    TRY(pin_malloc(reinterpret_cast<void **>(&h->h_stats), sizeof(DevStats)));
     for (auto &ev : h->ev) TRY(cudaEventCreate(&ev));
     TRY(cudaStreamSynchronize(h->st));
+    tmark("pools+rest");
 #undef TRY
     *out = h;
     return MP_OK;
@@ -1271,10 +1430,15 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     g_err.clear();
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
+    PinnedStage &stage = pinned_stage();
+    std::lock_guard<std::mutex> stage_lock(stage.mu);
     if (pair_duals) {
-        std::vector<double> a((size_t)h->m), b((size_t)h->m);
-        CK(cudaMemcpyAsync(a.data(), h->pu, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaMemcpyAsync(b.data(), h->pl, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        const size_t bytes = 2 * (size_t)h->m * sizeof(double);
+        double *a = static_cast<double *>(stage.get(bytes));
+        if (!a) return fail(MP_ERR_OOM, "pinned staging buffer");
+        double *b = a + h->m;
+        CK(cudaMemcpyAsync(a, h->pu, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(b, h->pl, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
         for (int64_t p = 0; p < h->m; ++p) {
             pair_duals[2 * p] = a[(size_t)p];
@@ -1284,12 +1448,16 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     if (!keys && !vals) return MP_OK;
     const DualPool &P = h->pool[h->rp];
     const int64_t used = h->pool_used[h->rp];
-    std::vector<ChunkRec> hr((size_t)used);
-    std::vector<int32_t> hh((size_t)h->nstreams);
+    const size_t rec_bytes = (size_t)used * sizeof(ChunkRec);
+    char *stg = static_cast<char *>(stage.get(rec_bytes + (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
+    if (!stg) return fail(MP_ERR_OOM, "pinned staging buffer");
+    const ChunkRec *hr = reinterpret_cast<const ChunkRec *>(stg);
+    const int32_t *hh = reinterpret_cast<const int32_t *>(stg + rec_bytes);
     if (used)
-        CK(cudaMemcpyAsync(hr.data(), P.rec, hr.size() * sizeof(ChunkRec), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(stg, P.rec, rec_bytes, cudaMemcpyDeviceToHost, h->st));
     if (h->nstreams)
-        CK(cudaMemcpyAsync(hh.data(), P.head, hh.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(stg + rec_bytes, P.head, (size_t)h->nstreams * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     const int64_t n = h->n;
     int64_t outpos = 0;
