@@ -199,6 +199,9 @@ struct CtaConst {
 __device__ __forceinline__ uint32_t mapa(uint32_t a, unsigned rank);
 __device__ __forceinline__ void st_cluster_f64(uint32_t a, double v);
 __device__ __forceinline__ bool forward_jk(const CtaConst *cc, uint32_t ue, double e) {
+#ifdef MP_EXP_NOFWD
+    return false;  // timing experiment only: results are wrong
+#endif
     const int C = cc->C, band = cc->band;
     int dlast = band;
     if (ue >= cc->rep_lo && ue < cc->zero_lo) {
@@ -617,6 +620,9 @@ __device__ __forceinline__ int32_t wr_alloc(const DualPool &p, PassCounters *ctr
 __device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassCounters *ctr,
                                           int64_t stream, uint32_t base, int lane, double t0,
                                           double t1, double t2) {
+#ifdef MP_EXP_NOAPPEND
+    return;  // timing experiment only: results are wrong
+#endif
     const bool h0 = t0 > THETA_FLOOR, h1 = t1 > THETA_FLOOR, h2 = t2 > THETA_FLOOR;
     const unsigned m0 = __ballot_sync(0xffffffffu, h0);
     const unsigned m1 = __ballot_sync(0xffffffffu, h1);
@@ -992,8 +998,11 @@ __device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, con
 // where cold_batch's live state would not fit the registers).  pa/pc/pe are
 // the slot's shared addresses (the zero row for inactive lanes).  Returns the
 // updated violation; `fwd` is set if a value was forwarded to a later band.
+#ifndef MP_SLOT_INLINE
+#define MP_SLOT_INLINE __noinline__
+#endif
 template <int W, bool UNIT>
-__device__ __noinline__ double cold_slot(const CtaConst *cc, WarpDuals *wd, int warp, uint32_t base,
+__device__ MP_SLOT_INLINE double cold_slot(const CtaConst *cc, WarpDuals *wd, int warp, uint32_t base,
                                          int pa, int pc, int pe, double viol, bool &fwd) {
     const int lane = threadIdx.x & 31;
     double y[1][3] = {{0.0, 0.0, 0.0}};
