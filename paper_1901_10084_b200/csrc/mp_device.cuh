@@ -453,6 +453,20 @@ __device__ __forceinline__ void tma_store_2d(const void *tmap, int c0, int c1, u
                  "r"(c0), "r"(c1), "r"(src)
                  : "memory");
 }
+// non-blocking test of an mbarrier phase
+__device__ __forceinline__ bool mbar_test(unsigned long long *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// bulk copy global -> own shared memory completing on `bar` (no expect_tx)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -1195,6 +1209,8 @@ struct TileSync {
     int hi_issued;      // producer's highest issued block (for the epilogue)
     int pslow, pfast;   // producer-internal broadcast
     int blk0;           // the tile's first ring block (TMA slot phases count from it)
+    int wb_lo;          // TMA producer: lowest block not yet written back (slots below are free)
+    int wslow;          // TMA producer: writers' broadcast of the slowest warp's next level
 };
 
 // Lowest ring block landed in every CTA of the cluster: a block may be used
@@ -1249,6 +1265,12 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
 
 #ifndef MP_BATCH
 #define MP_BATCH 8
+#endif
+#ifndef MP_LOOKAHEAD  // ring blocks loaded ahead of the fastest compute warp
+#define MP_LOOKAHEAD 4
+#endif
+#ifndef MP_OLD_PRODUCER  // 1: the cp.async producer also for TMA tiles (A/B only)
+#define MP_OLD_PRODUCER 0
 #endif
 
 // Sweep levels [La, Lb] of one phase.  Levels are taken in batches of U: in
@@ -1469,9 +1491,6 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
     const int blast = T.jhi / BLK;
     const uint32_t band0_done = C > 1 ? mapa(smem_u32(&ts->done[0]), 0) : 0u;
     const int nres = W / BLK;
-#ifndef MP_LOOKAHEAD
-#define MP_LOOKAHEAD 4
-#endif
     constexpr int LOOKAHEAD = MP_LOOKAHEAD;
     int landed = hi_issued;  // the prologue landed everything it issued
 #ifdef MP_TIMELINE
@@ -1595,6 +1614,124 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
     }
 }
 
+// Producer for tiles whose WK moves as TMA boxes (W = I): one elected loader
+// thread issues each block as one mbarrier transaction -- the WK box plus one
+// 128-byte bulk row copy per WR row of the band -- and publishes landed
+// blocks; two writer warps write back what the slowest compute warp passed.
+// The two roles run decoupled (the loader's capacity check reads the
+// writers' wb_lo), so a block's load never waits behind a write-back.
+template <int W>
+__device__ __noinline__ void ring_producer_tma(unsigned char *sm, const CtaConst *cc, TileSync *ts,
+                                               int nwc, int lo_res, int hi_issued) {
+    const TileDesc &T = cc->T;
+    const int b = cc->b, lane = threadIdx.x & 31;
+    const int ptid = threadIdx.x - nwc * 32;
+    double *smd = reinterpret_cast<double *>(sm);
+    const int C = cc->C, band = cc->band;
+    const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
+    const bool last_band = band == C - 1;
+    double *WR = smd, *WK = smd + SmemMap<W>{b, cc->RB, cc->wkp, cc->wrp}.wk() / 8;
+    const int blast = T.jhi / BLK;
+    constexpr int nres = W / BLK;
+    if (ptid < 32) {
+        if (lane != 0) return;
+        // ---- loader --------------------------------------------------------
+        const uint32_t band0_done = C > 1 ? mapa(smem_u32(&ts->done[0]), 0) : 0u;
+        const int rows = max(0, min(r1, T.ihi - T.ilo + 1) - r0);  // band rows that exist
+        const unsigned tx = (unsigned)(cc->wkp * BLK * 8 + rows * BLK * 8);
+        int landed = hi_issued, published = hi_issued;
+        while (true) {
+            int slow = 0x3fffffff, fast = -0x3fffffff;
+            for (int w = 0; w < nwc; ++w) {
+                const int v = ld_acquire(&ts->done[w]);
+                slow = min(slow, v);
+                fast = max(fast, v);
+            }
+            if (slow + 1 > T.Lend) break;
+            // band 0 leads the cluster: load ahead of it (a hint, relaxed)
+            if (C > 1) fast = max(fast, ld_relaxed_cluster(band0_done) + 2 * MP_BATCH);
+            const int need_fast = min(fast + 1 - T.ilo - T.klo, T.jhi) / BLK;
+            const int want = min(need_fast + MP_LOOKAHEAD, blast);
+            bool busy = false;
+            if (hi_issued < want) {
+                const int lo = ld_acquire(&ts->wb_lo);  // slots below lo were written back
+                if (hi_issued < want && hi_issued + 1 - lo < nres) fence_proxy_async();
+                while (hi_issued < want && hi_issued + 1 - lo < nres) {
+                    const int g = ++hi_issued;
+                    unsigned long long *bar = &ts->wkbar[g & (nres - 1)];
+                    mbar_expect_tx(bar, tx);
+                    tma_load_2d(smem_u32(WK + ((g * BLK) & (W - 1)) * cc->wkp), cc->tmap, T.klo, g * BLK, bar);
+                    const uint32_t wslot = smem_u32(WR + ((g * BLK) & (W - 1)));
+                    const double *src = cc->x + (int64_t)(T.ilo + r0) * cc->ld + g * BLK;
+                    for (int ii = 0; ii < rows; ++ii)
+                        bulk_g2s(wslot + (uint32_t)(ii * cc->wrp * 8), src + (int64_t)ii * cc->ld, BLK * 8, bar);
+                    busy = true;
+                }
+            }
+            // landed, in order; block only when the fastest warp needs the block next
+            while (landed < hi_issued) {
+                const int g = landed + 1;
+                const uint32_t ph = (uint32_t)(((g - ts->blk0) / nres) & 1);
+                if (!mbar_test(&ts->wkbar[g & (nres - 1)], ph)) {
+                    if (need_fast + 1 < g) break;
+                    mbar_wait(&ts->wkbar[g & (nres - 1)], ph);
+                }
+                landed = g;
+            }
+            if (landed > published) {
+                // the own CTA with a release (its warps read the ring), the
+                // others relaxed (back-pressure for their forwarded writes)
+                st_release(&ts->landed_by[band], landed);
+                for (int d = 0; d < C; ++d)
+                    if (d != band) st_relaxed_cluster(mapa(smem_u32(&ts->landed_by[band]), (unsigned)d), landed);
+                published = landed;
+                busy = true;
+            }
+            if (!busy) __nanosleep(32);
+        }
+        for (int g = landed + 1; g <= hi_issued; ++g)  // the epilogue writes every issued block back
+            mbar_wait(&ts->wkbar[g & (nres - 1)], (uint32_t)(((g - ts->blk0) / nres) & 1));
+        ts->hi_issued = hi_issued;
+        return;
+    }
+    // ---- writers (the other producer warps) ----------------------------------
+    const int wtid = ptid - 32, wn = 32 * (int)(blockDim.x / 32 - nwc - 1);
+    int lo = lo_res;
+    while (true) {
+        if (wtid < 32) {
+            int v = wtid < nwc ? ld_acquire(&ts->done[wtid]) : 0x3fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (wtid == 0) ts->wslow = v + 1;
+        }
+        asm volatile("bar.sync 2, %0;" ::"r"(wn) : "memory");
+        const int slow = ts->wslow;
+        if (slow > T.Lend) break;
+        const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
+        if (lo < low_need) {
+            for (; lo < low_need; ++lo) {
+                const bool st = last_band && wk_tma_store_ok(cc, lo);
+                ring_block<W, false>(T, b, cc->wkp, cc->wrp, cc->ld, cc->x, WR, WK, lo, wtid, wn, r0, r1,
+                                     last_band && !st);
+                if (st && wtid == 0) {
+                    fence_proxy_async();
+                    tma_store_2d(cc->tmap, T.klo, lo * BLK, smem_u32(WK + ((lo * BLK) & (W - 1)) * cc->wkp));
+                }
+            }
+            if (wtid == 0) bulk_wait_read_all();  // the box stores have read their slots
+            asm volatile("bar.sync 2, %0;" ::"r"(wn) : "memory");
+            if (wtid == 0) st_release(&ts->wb_lo, lo);
+        } else {
+            __nanosleep(64);
+        }
+        asm volatile("bar.sync 2, %0;" ::"r"(wn) : "memory");  // ts->wslow is rewritten next
+    }
+    if (wtid == 0) {
+        ts->lo_res = lo;
+        bulk_wait_all();  // box stores complete before the CTA exits
+    }
+}
+
 template <int S, int W, bool UNIT>
 __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1675,6 +1812,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const int hi0 = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
     if (tmap && tid == 0) {  // WK blocks by TMA (cc was written by this thread)
         ts.blk0 = lo0;
+        ts.wb_lo = lo0;
         for (int s = 0; s < W / BLK; ++s) mbar_init(&ts.wkbar[s], 1);
         mbar_fence_init();
         for (int bk = lo0; bk <= hi0; ++bk) wk_tma_load<W>(&cc, &ts, WK, bk);
@@ -1699,7 +1837,10 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 
     double viol = 0.0;
     if (warp >= nwc) {
-        ring_producer<W, UNIT>(sm, &cc, &ts, nwc, np, lo0, hi0);
+        if (UNIT && tmap && np >= 3 && !MP_OLD_PRODUCER)
+            ring_producer_tma<W>(sm, &cc, &ts, nwc, lo0, hi0);
+        else
+            ring_producer<W, UNIT>(sm, &cc, &ts, nwc, np, lo0, hi0);
     } else {
         // --- per-slot geometry: q = warp*32*S + s*32 + lane -> (i,k) -------
         SlotGeom<S> G;
