@@ -1837,7 +1837,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 
     double viol = 0.0;
     if (warp >= nwc) {
-        if (UNIT && tmap && np >= 3 && !MP_OLD_PRODUCER)
+        // (one CTA per tile: 40 WR rows per block are too many bulk copies for
+        // one loader thread; the combined producer is faster there, config 5)
+        if (UNIT && tmap && np >= 3 && C > 1 && !MP_OLD_PRODUCER)
             ring_producer_tma<W>(sm, &cc, &ts, nwc, lo0, hi0);
         else
             ring_producer<W, UNIT>(sm, &cc, &ts, nwc, np, lo0, hi0);

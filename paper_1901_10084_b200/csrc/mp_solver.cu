@@ -606,11 +606,26 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
     const int slots = c.RB * b;
     int S = 1;
     if (const char *e = getenv("MP_SLOTS")) S = std::max(S, atoi(e));
+    // Column-major bands: a warp holds whole columns (LW a multiple of RB).  A
+    // column split over two warps couples them through the in-column lattice
+    // dependency and every exact step of the column stalls both (config 2, RB
+    // = 5: LW = 30 is 8% faster than 32; 20 equals 30; 16 or 15 is slower).
+    // Taken only when it needs no more slots per thread and leaves room for
+    // three producer warps (else 32 lanes: config 3's C = 2 and C = 4 rounds).
+    auto slots_per_thread = [&](int lw) {
+        int s = S;
+        while ((slots + lw * s - 1) / (lw * s) > MAX_CTA_THREADS / 32 - 1) ++s;
+        return s;
+    };
     c.LW = 32;
+    if (c.colm && C > 1 && c.RB <= 32) {
+        const int lw = c.RB * (32 / c.RB), s = slots_per_thread(lw);
+        if (s <= slots_per_thread(32) && (slots + lw * s - 1) / (lw * s) <= MAX_CTA_THREADS / 32 - 3) c.LW = lw;
+    }
     if (const char *e = getenv("MP_LANES"))  // cluster rounds only (one CTA needs them all)
         if (C > 1) c.LW = std::max(1, std::min(32, atoi(e)));
     const int LW = c.LW;
-    while ((slots + LW * S - 1) / (LW * S) > MAX_CTA_THREADS / 32 - 1) ++S;
+    S = slots_per_thread(LW);
     c.S = S;
     c.NWC = (slots + LW * S - 1) / (LW * S);
     c.NPW = std::min(3, MAX_CTA_THREADS / 32 - c.NWC);
