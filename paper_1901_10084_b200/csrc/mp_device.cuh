@@ -190,6 +190,9 @@ struct CtaConst {
     int32_t wrp;          // WR row pitch (doubles)
 };
 
+#ifndef MP_CMAX  // largest cluster (CTAs per tile) the host plans; > 8 is non-portable
+#define MP_CMAX 8
+#endif
 // Forwarding of an exact step's x_jk write to the later bands that read it
 // (a cluster CTA's x_ij and x_ik lie in its own rows, which no later band
 // reads): a WK value is read by every later band, an RK value (row j of the
@@ -211,7 +214,7 @@ __device__ __forceinline__ bool forward_jk(const CtaConst *cc, uint32_t ue, doub
         dlast = min(C - 1, (int)((row * cc->band_mul) >> 16));
     }
 #pragma unroll
-    for (int d = 1; d < 8; ++d)
+    for (int d = 1; d < MP_CMAX; ++d)  // (unrolled to the largest cluster the host plans)
         if (band + d <= dlast) st_cluster_f64(mapa(ue, (unsigned)(band + d)), e);
     return dlast > band;
 }
@@ -1791,7 +1794,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.tma_st = T.z - T.klo + 1 == b;
         cc.wkp = a.wkp;
         cc.wrp = a.wrp;
-        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0;
+        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0 && band < 8;
         cc.B32 = B32;
         cc.lw = a.lw;
         cc.colm = a.colm;

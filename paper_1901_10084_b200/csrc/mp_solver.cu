@@ -35,6 +35,7 @@
 
 using namespace mp;
 
+
 namespace {
 
 thread_local std::string g_err;
@@ -517,6 +518,9 @@ int smem_optin(const void *k, size_t bytes) {
             return MP_OK;
         }
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    // clusters of up to 16 CTAs (beyond the portable 8) in -DMP_CMAX=16 builds:
+    // C = 10 / 14 bands were no faster than C = 8 at config 2
+    if (MP_CMAX > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cur.push_back({{k, dev}, bytes});
     return MP_OK;
 }
@@ -686,11 +690,11 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const mp_handle::RoundCfg one = round_shape(h, 1);
-    int cmax = 8;
-    if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(8, atoi(e)));
-    std::vector<int> cap(9, -1);  // co-resident clusters per C (queried once)
-    std::vector<mp_handle::RoundCfg> shape(9);  // launch shape per C (computed once)
-    std::vector<bool> have(9, false);
+    int cmax = MP_CMAX;
+    if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(MP_CMAX, atoi(e)));
+    std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
+    std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
+    std::vector<bool> have(17, false);
     h->rcfg.clear();
     for (size_t r = 0; r < cnt_r.size(); ++r) {
         const int64_t cnt = cnt_r[r];
@@ -710,10 +714,10 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         h->rcfg.push_back(best);
     }
     if (getenv("MP_VERBOSE")) {
-        std::vector<int> hist(9, 0);
+        std::vector<int> hist(17, 0);
         for (const auto &c : h->rcfg) hist[(size_t)c.C]++;
         fprintf(stderr, "[mp] n=%lld b=%d rounds by cluster size:", (long long)h->n, b);
-        for (int C = 1; C <= 8; ++C)
+        for (int C = 1; C <= 16; ++C)
             if (hist[(size_t)C]) {
                 const mp_handle::RoundCfg c = round_shape(h, C);
                 fprintf(stderr, " C=%d:%d (S=%d NWC=%d NT=%d W=%d P=%d PR=%d smem=%zu cap=%d)", C, hist[(size_t)C],
