@@ -61,10 +61,16 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._drain, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first
+            # sample so the (short) timed region is sampled from its start
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.n0 = len(self.lines)
         except OSError:
             self.proc = None
         return self
@@ -75,6 +81,10 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc is not None:
+            # at least one sample taken after the region started
+            t0 = time.time()
+            while len(self.lines) <= getattr(self, "n0", 0) and time.time() - t0 < 2.0 and self.proc.poll() is None:
+                time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -84,7 +94,8 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples from the timed region (the first one was taken before it)
+        for ln in (self.lines[getattr(self, "n0", 0):] or self.lines):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue

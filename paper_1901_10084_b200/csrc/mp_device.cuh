@@ -60,6 +60,16 @@ namespace mp {
 
 constexpr double THETA_FLOOR = 1e-15;  // _kernels.py:20
 constexpr int BLK = 16;                // j-block width of the streamed rings
+// levels per progress publish (batch) of a compute warp
+#ifndef MP_BATCH
+#define MP_BATCH 8
+#endif
+#ifndef MP_LOOKAHEAD  // ring blocks loaded ahead of the fastest compute warp
+#define MP_LOOKAHEAD 4
+#endif
+#ifndef MP_OLD_PRODUCER  // 1: the cp.async producer also for TMA tiles (A/B only)
+#define MP_OLD_PRODUCER 0
+#endif
 constexpr int CHUNK = 32;              // dual entries per pool chunk
 constexpr uint32_t KEY_END = 0xFFFFFFFFu;
 constexpr int MAX_CTA_THREADS = 512;   // >= 128 registers per thread
@@ -1089,14 +1099,20 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
     const StepConsts k = cc->kc;
     const int xb = cc->xsize * 8;  // winv staging mirrors the x layout (general W)
     const bool fwd_band = C > 1 && band + 1 < C;
-    bool dirty = false, fwd = false;
+    bool fwd = false;
+    // Levels left to replay: bit Lc - L0 set when some lane's row at Lc is
+    // violated.  After a level that moved x the later levels are re-checked
+    // with the new values (the hot test, all of them at once) instead of being
+    // replayed one by one -- a replayed level with no violated row and no
+    // stored dual is a no-op in the reference.
+    unsigned todo = flagged;
 #ifdef MP_TIMELINE
     long long tq0 = clock64(), c_lk = 0, c_mt = 0, c_ap = 0, c_ld = 0, nlev = 0;
 #endif
     for (int Lc = first; Lc <= Le; ++Lc) {
         const uint32_t base = (uint32_t)(Lc - T.Lbeg) * PER_LEVEL;
         const bool has_dual = wd->head < base + PER_LEVEL;
-        if (!dirty && !has_dual && !((flagged >> (Lc - L0)) & 1u)) continue;
+        if (!has_dual && !((todo >> (Lc - L0)) & 1u)) continue;
 #ifdef MP_TIMELINE
         ++nlev;
         long long tq = clock64();
@@ -1148,7 +1164,21 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
             { const long long t = clock64(); c_ap += t - tq; tq = t; }
 #endif
         }
-        dirty |= __any_sync(0xffffffffu, moved);
+        if (__any_sync(0xffffffffu, moved) && Lc < Le) {
+            unsigned f = 0;
+#pragma unroll
+            for (int u = 1; u < MP_BATCH; ++u) {
+                const int Lx = Lc + u;
+                if (Lx <= Le) {  // warp-uniform
+                    int qa[S], qc[S], qe[S];
+                    slot_addrs<S, W, ALIAS>(G, Lx, b, T.ihi, T.klo, qa, qc, qe);
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+                        f |= triplet_violated(ld_sh(qa[s]), ld_sh(qc[s]), ld_sh(qe[s])) << (Lx - L0);
+                }
+            }
+            todo = (todo & ((2u << (Lc - L0)) - 1u)) | __reduce_or_sync(0xffffffffu, f);
+        }
     }
 #ifdef MP_TIMELINE
     if (cc->tl && lane == 0) {  // the caller's batch record, slots 4..7
@@ -1266,15 +1296,6 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
     return ld_acquire_cluster(a);
 }
 
-#ifndef MP_BATCH
-#define MP_BATCH 8
-#endif
-#ifndef MP_LOOKAHEAD  // ring blocks loaded ahead of the fastest compute warp
-#define MP_LOOKAHEAD 4
-#endif
-#ifndef MP_OLD_PRODUCER  // 1: the cp.async producer also for TMA tiles (A/B only)
-#define MP_OLD_PRODUCER 0
-#endif
 
 // Sweep levels [La, Lb] of one phase.  Levels are taken in batches of U: in
 // the common case nothing moves, so the U levels' checks read only data
