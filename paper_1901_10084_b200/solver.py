@@ -308,11 +308,21 @@ def solve(instance, config=None, stats_stream=None):
     budget = config.fixed_passes if config.fixed_passes is not None else config.max_passes
     stats, total, converged = [], 0, False
     try:
-        for k in range(budget):
+        if config.fixed_passes is not None and stats_stream is None:
+            # benchmark mode: every pass in one native call (no host round trip
+            # per pass); the native loop stops at the first non-finite pass
             try:
-                raw = sess.run(1)[0]
-            except SolverError:
-                raise SolverError(f"non-finite value in state after pass {k}") from None
+                raws = sess.run(budget)
+            except SolverError as e:
+                raise SolverError(str(e)) from None
+        for k in range(budget):
+            if config.fixed_passes is not None and stats_stream is None:
+                raw = raws[k]
+            else:
+                try:
+                    raw = sess.run(1)[0]
+                except SolverError:
+                    raise SolverError(f"non-finite value in state after pass {k}") from None
             st = _to_stats(raw, k)
             stats.append(st)
             total += st.steps
