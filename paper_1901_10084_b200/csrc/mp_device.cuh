@@ -2,7 +2,9 @@
 //
 // Hot path: the reference's metric_units_pass (_kernels.py:60-132) executed
 // for one round of conflict-free tiles (schedule.tiled_rounds,
-// schedule.py:117-153) as ONE launch, one CTA per tile.
+// schedule.py:117-153) as ONE launch: one thread-block cluster of C CTAs per
+// tile (CTA `band` owns tile rows [band*RB, band*RB + RB)), or one CTA per
+// tile when a round has more tiles than clusters fit.
 //
 // Order exactness.  Two triplets conflict iff they share two indices; their
 // index sums L = i+j+k then differ, and inside one round the reference's
@@ -10,37 +12,40 @@
 // visits the conflicting triplet with the smaller L first.
 // Sweeping a tile level by level in L, any order inside a level, is
 // therefore a linear extension of the reference order and reproduces its x
-// bit for bit.  Each CTA walks its tile's L-levels with one __syncthreads()
-// per level; thread slot q owns the pair (i,k) = (ilo + q/b, klo + q%b) and
-// at level L processes the triplet (i, L-i-k, k), all three rows in kind
-// order IJ, IK, JK (_kernels.py:97-109).
+// bit for bit.  Thread slot (i,k) processes the triplet (i, L-i-k, k) at
+// level L, all three rows in kind order IJ, IK, JK (_kernels.py:97-109).
+// There are no per-level barriers: every conflict is ordered along the (i,k)
+// lattice, so a warp only waits (per batch of MP_BATCH levels) for the warp
+// holding its left columns and, in the previous band, the warp above it
+// (see sweep()); warps of a band hold whole columns.
 //
 // Shared-memory layout of one tile (R = [ilo,ihi] rows i, K = [klo,z]
-// columns k, J = [jlo,jhi] middle indices):
+// columns k, J = [jlo,jhi] middle indices; SmemMap):
+//   WR[rows][W]   x_ij, i in the band's rows, j in J, j < klo  -- ring over j
+//   WK[W][b]      x_jk, j in J, j > ihi, k in K  -- ring over j, in x's row
+//                 order (a 16-row block is one 2-D TMA box), replicated in
+//                 every band, later bands receive exact-step writes by DSMEM
 //   RK[b][b]      every pair (a,c) with a in R and c in K  (canonical home,
 //                 so x_ij with j in K and x_jk with j in R alias into it)
-//   WR[b][W]      x_ij, i in R, j in J, j < klo  -- ring over j, slot j%W
-//   WK[W][b]      x_jk, j in J, j > ihi, k in K  -- ring over j, row j%W
-// The rings are streamed from the dense (n x ld) x matrix in j-blocks of
-// BLK columns with cp.async one block ahead of the wavefront, and written
-// back when the wavefront has passed them.  Each pair touched by a tile is
-// touched by no other tile of the round (schedule.py:235-250), so no two
-// CTAs of a launch ever write the same x.
+// Row pitches of WR and WK are padded against bank conflicts (host-chosen).
+// The rings are streamed from the dense (n x ld) x matrix in blocks of BLK
+// j-values ahead of the fastest warp (TMA box + bulk row copies, or
+// cp.async) and written back behind the slowest.  Each pair touched by a
+// tile is touched by no other tile of the round (schedule.py:235-250), so no
+// two clusters of a launch ever write the same x.
 //
 // Hot / cold split.  In the common case a row is neither violated nor has a
 // stored dual, and the reference step is then a no-op (delta = d0 <= 0 ->
-// theta = coef = 0).  The hot loop therefore only loads the three x values,
-// forms the three row values with six DADDs and tests them; a warp that
-// finds a violated row or reaches a stored dual calls the out-of-line
-// cold_level(), which replays the level for its slots with the full
-// reference step.  Keeping the IEEE divisions and the dual bookkeeping out
-// of line keeps the hot loop's register footprint small.
+// theta = coef = 0).  The hot loop therefore only loads x_ij and x_jk (x_ik
+// is register-held in the alias-free middle of a tile) and tests the rows
+// with two DADDs; a batch with a violated row or a stored dual runs the exact
+// reference step for the levels that need it (cold_batch / cold_slot).
 //
 // Arithmetic mirrors the reference bit for bit: explicit __dadd_rn /
-// __dsub_rn / __dmul_rn / __ddiv_rn (no FMA contraction) in the reference's
-// association (_kernels.py:115-125).  When W = I (reg_x == 1) the weights
-// are exactly 1.0 and s = (1+1)+1 = 3 exactly, so the UNIT specialisation
-// is bitwise identical to the general path.
+// __dsub_rn / __dmul_rn and IEEE-exact division (no FMA contraction) in the
+// reference's association (_kernels.py:115-125).  When W = I (reg_x == 1)
+// the weights are exactly 1.0 and s = (1+1)+1 = 3 exactly, so the UNIT
+// specialisation is bitwise identical to the general path.
 //
 // Sparse duals: each warp of each tile owns one "stream" of its nonzero
 // duals, a linked list of 32-entry chunk records in a global pool.  Entries
