@@ -1411,13 +1411,23 @@ int mp_get_state(mp_handle *h, double *xv, double *fv) {
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
     const int g = grid_for(h->m, 256, 148 * 16);
+    // through the pinned staging buffer (a pageable copy runs at a fraction
+    // of the link rate)
+    PinnedStage &stage = pinned_stage();
+    std::lock_guard<std::mutex> stage_lock(stage.mu);
+    const size_t mb = (size_t)h->m * sizeof(double);
+    char *stg = static_cast<char *>(stage.get(2 * mb));
     if (xv) {
         pack_kernel<<<g, 256, 0, h->st>>>(h->x, h->tmp, h->ld, h->n, h->m);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(xv, h->tmp, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(stg ? (void *)stg : (void *)xv, h->tmp, mb, cudaMemcpyDeviceToHost, h->st));
     }
-    if (fv) CK(cudaMemcpyAsync(fv, h->f, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    if (fv) CK(cudaMemcpyAsync(stg ? (void *)(stg + mb) : (void *)fv, h->f, mb, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    if (stg) {
+        if (xv) std::memcpy(xv, stg, mb);
+        if (fv) std::memcpy(fv, stg + mb, mb);
+    }
     return MP_OK;
 }
 
