@@ -847,17 +847,45 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int 
     }
 }
 
-// RK block: rows i in R (relative rows [r0, r1)), columns k in K, i < k.
+// RK block: rows i in R (relative rows [r0, r1)), columns k in K, i < k.  A
+// warp takes a row, lanes over k; with klo and b even, 16-byte pairs (both
+// sides aligned: RK rows are b doubles, x rows ld).
 template <bool LOAD>
 __device__ __forceinline__ void rk_block(const TileDesc &T, int b, int64_t ld, double *g,
                                          double *rk, int tid, int nt, int r0, int r1) {
-    for (int e = r0 * b + tid; e < r1 * b; e += nt) {
-        const int ii = e / b, kk = e - ii * b;
-        const int i = T.ilo + ii, k = T.klo + kk;
-        if (i <= T.ihi && k <= T.z && i < k) {
-            double *gp = g + (int64_t)i * ld + k;
-            if (LOAD) cp_async8(rk + e, gp);
-            else *gp = rk[e];
+    const int lane = tid & 31, nw = nt >> 5;
+    const bool pairs = !((T.klo | b) & 1);
+    for (int ii = r0 + (tid >> 5); ii < r1; ii += nw) {
+        const int i = T.ilo + ii;
+        if (i > T.ihi) continue;  // warp-uniform
+        double *grow = g + (int64_t)i * ld + T.klo;
+        const uint32_t srow = smem_u32(rk + ii * b);
+        if (pairs) {
+            for (int kk = 2 * lane; kk < b; kk += 64) {
+                const int k = T.klo + kk;
+                const bool v0 = k <= T.z && i < k, v1 = kk + 1 < b && k + 1 <= T.z && i < k + 1;
+                if (v0 & v1) {
+                    if (LOAD) cp_async16(srow + 8 * kk, grow + kk);
+                    else st_global_v2(grow + kk, srow + 8 * kk);
+                } else {
+                    if (v0) {
+                        if (LOAD) cp_async8s(srow + 8 * kk, grow + kk);
+                        else grow[kk] = ld_sh(srow + 8 * kk);
+                    }
+                    if (v1) {
+                        if (LOAD) cp_async8s(srow + 8 * kk + 8, grow + kk + 1);
+                        else grow[kk + 1] = ld_sh(srow + 8 * kk + 8);
+                    }
+                }
+            }
+        } else {
+            for (int kk = lane; kk < b; kk += 32) {
+                const int k = T.klo + kk;
+                if (k <= T.z && i < k) {
+                    if (LOAD) cp_async8s(srow + 8 * kk, grow + kk);
+                    else grow[kk] = ld_sh(srow + 8 * kk);
+                }
+            }
         }
     }
 }
