@@ -57,7 +57,36 @@ class ClockSampler:
         self.proc = None
         self.lines = []
 
+    def _nvml_loop(self, h, nv):
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            flags = ", ".join("Active" if r & bt else "Not Active" for bt in bits)
+            self.lines.append(f"{sm}, {mx}, {r:#x}, {flags}")
+            self.stop.wait(0.005)
+
     def __enter__(self):
+        # in-process NVML sampling every 5 ms (the timed region is ~0.1-1 s);
+        # nvidia-smi -lms 50 as the fallback when NVML is not importable
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(h, nv), daemon=True)
+            self.thread.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 2.0:
+                time.sleep(0.001)
+            self.n0 = len(self.lines)
+            self.nvml = True
+            return self
+        except Exception:
+            self.nvml = False
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -80,6 +109,14 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if getattr(self, "nvml", False):
+            n = len(self.lines)
+            t0 = time.time()
+            while len(self.lines) <= n and time.time() - t0 < 0.5:
+                time.sleep(0.001)
+            self.stop.set()
+            self.thread.join(timeout=2)
+            return
         if self.proc is not None:
             # at least one sample taken after the region started
             t0 = time.time()
