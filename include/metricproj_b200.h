@@ -176,6 +176,17 @@ int mp_group_run_passes(mp_handle *const *hs, int32_t world, int32_t npasses, mp
 int mp_max_violation(int64_t n, const double *xv, const double *fv, const double *d_flat,
                      double *out);
 
+/* Kernel-level drop-in for core.accumulate_aty(instance, duals)
+ * (core.py:285-293): g = c + A^T y over the stored duals, host buffers in and
+ * out.  keys[nnz] = ConstraintKey.encode codes (core.py:81-85) with vals[nnz]
+ * in DualStore.items() order; pair_duals = [C(n,2)][2] (upper, lower);
+ * c = instance.c_vector() (length 2 C(n,2)); g receives 2 C(n,2) values, bit
+ * for bit the reference's sequential accumulation (per target, contributions
+ * in items() order).  Runs on the current CUDA device; invalid key ->
+ * MP_ERR_ARG. */
+int mp_accumulate_aty(int64_t n, int64_t nnz, const int64_t *keys, const double *vals,
+                      const double *pair_duals, const double *c, double *g);
+
 /* Correlation-clustering instance of a graph (instance.cc_instance,
  * instance.py:124-161): closed-neighbourhood Jaccard J of every pair (the
  * sparse product B*B^T on the device), s = log((1 + J - guard) / (1 - J +

@@ -331,3 +331,62 @@ def cc_instance_np(rowptr, cols, n, offset=0.01, guard=0.05, cap=10.0):
     s = np.where(s >= 0, s + offset, s - offset)
     iu = np.triu_indices(n, 1)
     return np.where(s < 0, 1.0, 0.0)[iu], np.abs(s)[iu]
+
+
+def accumulate_aty_loop(n, keys, vals, pair_duals, c):
+    """c + A^T y exactly as core.accumulate_aty (core.py:285-293) does it:
+    ``DualStore.items()`` order (metric keys in store order, then the pair
+    duals upper/lower per pair, core.py:244-253), each row's entries in
+    ``_row_entries`` order (core.py:296-311), ``g[pos] += coef * y``.  Pure
+    Python: tiny n only."""
+    g = np.array(c, dtype=np.float64, copy=True)
+    m = pair_count(n)
+    for code, y in zip(keys, vals):
+        code = int(code)
+        kind, t3 = code % 3, code // 3
+        i, j, k = t3 // (n * n), (t3 // n) % n, t3 % n
+        pij, pik, pjk = _pos(n, i, j), _pos(n, i, k), _pos(n, j, k)
+        ent = {0: ((pij, 1.0), (pik, -1.0), (pjk, -1.0)),
+               1: ((pik, 1.0), (pij, -1.0), (pjk, -1.0)),
+               2: ((pjk, 1.0), (pij, -1.0), (pik, -1.0))}[kind]
+        for pos, coef in ent:
+            g[pos] += coef * float(y)
+    for p in range(m):
+        yu, yl = float(pair_duals[p, 0]), float(pair_duals[p, 1])
+        if yu != 0.0:
+            g[p] += 1.0 * yu
+            g[m + p] += -1.0 * yu
+        if yl != 0.0:
+            g[p] += -1.0 * yl
+            g[m + p] += -1.0 * yl
+    return g
+
+
+def accumulate_aty_np(n, keys, vals, pair_duals, c):
+    """Vectorised restatement of :func:`accumulate_aty_loop` with the same
+    per-position addition order: ``np.add.at`` is unbuffered and sequential,
+    so feeding it the row entries interleaved key by key (3e, 3e+1, 3e+2)
+    reproduces the reference's loop bit for bit."""
+    g = np.array(c, dtype=np.float64, copy=True)
+    m = pair_count(n)
+    keys = np.asarray(keys, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    if len(keys):
+        kind, t3 = keys % 3, keys // 3
+        i, j, k = t3 // (n * n), (t3 // n) % n, t3 % n
+        rs = lambda a: a * (n - 1) - a * (a - 1) // 2  # noqa: E731
+        pij, pik, pjk = rs(i) + j - i - 1, rs(i) + k - i - 1, rs(j) + k - j - 1
+        plus = np.where(kind == 0, pij, np.where(kind == 1, pik, pjk))
+        m1 = np.where(kind == 0, pik, pij)
+        m2 = np.where(kind == 2, pik, pjk)
+        tgt = np.stack([plus, m1, m2], axis=1).ravel()
+        sv = np.stack([vals, -vals, -vals], axis=1).ravel()
+        np.add.at(g, tgt, sv)
+    yu, yl = pair_duals[:, 0], pair_duals[:, 1]
+    gx, gf = g[:m], g[m:]
+    nu, nl = yu != 0.0, yl != 0.0
+    gx[nu] += yu[nu]
+    gf[nu] += -yu[nu]
+    gx[nl] += -yl[nl]
+    gf[nl] += -yl[nl]
+    return g

@@ -96,7 +96,7 @@ EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dua
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
            "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_check_division",
            "mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
-           "mp_group_run_passes", "mp_cc_instance", "mp_last_error", "mp_version")
+           "mp_group_run_passes", "mp_cc_instance", "mp_accumulate_aty", "mp_last_error", "mp_version")
 
 _lib = None
 
@@ -147,6 +147,8 @@ def load():
     L.mp_destroy.restype = None
     L.mp_destroy.argtypes = [P]
     L.mp_max_violation.argtypes = [ctypes.c_int64, D, D, D, D]
+    L.mp_accumulate_aty.argtypes = [ctypes.c_int64, ctypes.c_int64, I, D, D, D, D]
+    L.mp_accumulate_aty.restype = ctypes.c_int
     L.mp_check_division.argtypes = [ctypes.c_double, ctypes.c_int64, ctypes.c_uint64, I]
     L.mp_check_division.restype = ctypes.c_int
     L.mp_get_duals_ranked.argtypes = [P, I, D, I]

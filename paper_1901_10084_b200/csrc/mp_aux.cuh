@@ -244,6 +244,80 @@ __global__ void reciprocal_kernel(const double *in, double *out, int64_t m) {
 }
 
 // ---------------------------------------------------------------------------
+// g = c + A^T y from stored duals (core.accumulate_aty, core.py:285-293;
+// SURVEY.md 8(f) rank 3).  The reference adds, per target position, the
+// contributions of the stored duals in DualStore.items() order (metric keys in
+// store order, three row entries each: core.py:296-311), then the pair duals
+// (upper, then lower, core.py:244-253).  The device reproduces that order
+// bit for bit: one record per metric row entry (record r = 3e + slot), a
+// stable radix sort of the records by target keeps r ascending inside a
+// target, and one thread per target segment adds sequentially from g = c.
+// ---------------------------------------------------------------------------
+// keys -> (target, record) pairs; slot 0 is the +1 entry, slots 1, 2 the -1s
+__global__ void aty_records_kernel(const int64_t *keys, int64_t nnz, int64_t n, uint32_t *tgt,
+                                   uint32_t *rec, int *bad) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t code = keys[e];
+        const int64_t kind = code % 3, t3 = code / 3;
+        const int64_t k = t3 % n, j = (t3 / n) % n, i = t3 / (n * n);
+        if (code < 0 || !(i < j && j < k && k < n)) {
+            atomicExch(bad, 1);
+            tgt[3 * e] = tgt[3 * e + 1] = tgt[3 * e + 2] = 0;
+        } else {
+            const int64_t pij = row_start(n, i) + (j - i - 1);
+            const int64_t pik = row_start(n, i) + (k - i - 1);
+            const int64_t pjk = row_start(n, j) + (k - j - 1);
+            // METRIC_IJ (pij, pik, pjk), METRIC_IK (pik, pij, pjk), METRIC_JK (pjk, pij, pik)
+            tgt[3 * e] = (uint32_t)(kind == 0 ? pij : (kind == 1 ? pik : pjk));
+            tgt[3 * e + 1] = (uint32_t)(kind == 0 ? pik : pij);
+            tgt[3 * e + 2] = (uint32_t)(kind == 2 ? pik : pjk);
+        }
+        rec[3 * e] = (uint32_t)(3 * e);
+        rec[3 * e + 1] = (uint32_t)(3 * e + 1);
+        rec[3 * e + 2] = (uint32_t)(3 * e + 2);
+    }
+}
+
+// g[0:m] = c[0:m] + metric contributions (sorted records), one thread per
+// target segment, sequential in record order; coef * y is y or -y exactly
+__global__ void aty_segments_kernel(const uint32_t *tgt, const uint32_t *rec, int64_t nrec,
+                                    const double *vals, double *g) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nrec;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = tgt[t];
+        if (t > 0 && tgt[t - 1] == p) continue;
+        double acc = g[p];
+        for (int64_t u = t; u < nrec && tgt[u] == p; ++u) {
+            const uint32_t r = rec[u];
+            const double y = vals[r / 3];
+            acc = __dadd_rn(acc, (r % 3 == 0) ? y : -y);
+        }
+        g[p] = acc;
+    }
+}
+
+// pair rows after every metric row (items() order): upper (p: +yu, m+p: -yu)
+// then lower (p: -yl, m+p: -yl); zero duals are not stored, so not added
+__global__ void aty_pairs_kernel(const double *pd, const double *c, double *g, int64_t m) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const double yu = pd[2 * p], yl = pd[2 * p + 1];
+        double gx = g[p], gf = c[m + p];
+        if (yu != 0.0) {
+            gx = __dadd_rn(gx, yu);
+            gf = __dadd_rn(gf, -yu);
+        }
+        if (yl != 0.0) {
+            gx = __dadd_rn(gx, -yl);
+            gf = __dadd_rn(gf, -yl);
+        }
+        g[p] = gx;
+        g[m + p] = gf;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // correlation-clustering instance from a graph (instance.cc_instance,
 // instance.py:124-161)
 // ---------------------------------------------------------------------------

@@ -11,6 +11,7 @@
 // reads the pool pass k-1 wrote (SPEC.md "read pass k-1, write pass k").
 #include <cuda.h>  // CUtensorMap (the encoder is resolved through the runtime)
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the functions are resolved at run time (nccl_api)
 
@@ -2039,6 +2040,73 @@ int mp_max_violation(int64_t n, const double *xv, const double *fv, const double
     double v;
     std::memcpy(&v, &bits, sizeof(v));
     *out = v;
+    return MP_OK;
+}
+
+int mp_accumulate_aty(int64_t n, int64_t nnz, const int64_t *keys, const double *vals,
+                      const double *pair_duals, const double *c, double *g) {
+    g_err.clear();
+    if (n < 3 || nnz < 0 || (nnz > 0 && (!keys || !vals)) || !pair_duals || !c || !g)
+        return fail(MP_ERR_ARG, "bad argument");
+    const int64_t m = pair_count(n);
+    if (2 * m > (int64_t)UINT32_MAX || 3 * nnz > (int64_t)INT32_MAX)
+        return fail(MP_ERR_ARG, "accumulate_aty: sizes beyond 32-bit record indices");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MP_ERR_CUDA, "no CUDA device available; there is no CPU fallback");
+    const int nrec = (int)(3 * nnz);
+    int end_bit = 1;
+    while (end_bit < 32 && ((int64_t)1 << end_bit) < m) ++end_bit;
+    double *dg = nullptr, *dc = nullptr, *dpd = nullptr, *dv = nullptr;
+    int64_t *dk = nullptr;
+    uint32_t *t0 = nullptr, *t1 = nullptr, *r0 = nullptr, *r1 = nullptr;
+    int *bad = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    auto cleanup = [&]() {
+        for (void *q : {(void *)dg, (void *)dc, (void *)dpd, (void *)dv, (void *)dk, (void *)t0,
+                        (void *)t1, (void *)r0, (void *)r1, (void *)bad, tmp})
+            cudaFree(q);
+        cudaStreamDestroy(st);
+    };
+    cudaError_t e = cudaSuccess;
+    const size_t nr = (size_t)std::max(nrec, 1);
+    if (nrec > 0)
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, t0, t1, r0, r1, nrec, 0, end_bit, st);
+    if ((e = cudaMalloc(&dg, 2 * m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dc, 2 * m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dpd, 2 * m * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dv, std::max<int64_t>(nnz, 1) * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dk, std::max<int64_t>(nnz, 1) * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&t0, nr * 4)) != cudaSuccess || (e = cudaMalloc(&t1, nr * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&r0, nr * 4)) != cudaSuccess || (e = cudaMalloc(&r1, nr * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&bad, sizeof(int))) != cudaSuccess ||
+        (e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16))) != cudaSuccess) {
+        cleanup();
+        return fail(MP_ERR_OOM, "cudaMalloc: %s", cudaGetErrorString(e));
+    }
+    cudaMemcpyAsync(dc, c, 2 * m * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dg, dc, m * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(dpd, pair_duals, 2 * m * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    if (nnz > 0) {
+        cudaMemcpyAsync(dk, keys, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(dv, vals, nnz * sizeof(double), cudaMemcpyHostToDevice, st);
+        aty_records_kernel<<<grid_for(nnz, 256, 148 * 16), 256, 0, st>>>(dk, nnz, n, t0, r0, bad);
+        cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, t0, t1, r0, r1, nrec, 0, end_bit, st);
+        aty_segments_kernel<<<grid_for(nrec, 256, 148 * 16), 256, 0, st>>>(t1, r1, nrec, dv, dg);
+    }
+    aty_pairs_kernel<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(dpd, dc, dg, m);
+    int hbad = 0;
+    cudaMemcpyAsync(g, dg, 2 * m * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cleanup();
+    if (e != cudaSuccess) return fail(MP_ERR_CUDA, "accumulate_aty: %s", cudaGetErrorString(e));
+    if (hbad) return fail(MP_ERR_ARG, "invalid metric key");
     return MP_OK;
 }
 

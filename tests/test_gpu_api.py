@@ -159,3 +159,48 @@ def test_worked_example():
     assert abs(x[core.pair_index(3, 0, 2)] - 1 / 3) <= 1e-15
     keys, vals, _ = sess.duals()
     assert len(keys) == 1 and abs(vals[0] - eps / 3) <= 1e-15
+
+
+def test_accumulate_aty_bitwise_reference_golden():
+    """mp_accumulate_aty = core.accumulate_aty (core.py:285-293) bit for bit on
+    the reference's own outputs (tests/golden/aty.npz: a random two-worker
+    store and the reference's duals after 6 passes of config 1), and
+    dual_objective (core.py:320-327) on top of it."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "aty.npz"))
+    for p in ("r", "c"):
+        n = int(z[p + "_n"])
+        inst = instances.random_instance(n, seed=7) if p == "r" else instances.config_instance(1)
+        assert np.array_equal(inst.c_vector(), z[p + "_c"])
+        d = core.DualStore(n, 1)
+        d.keys, d.vals = [z[p + "_keys"]], [z[p + "_vals"]]
+        d.pair_duals = z[p + "_pd"].copy()
+        assert np.array_equal(core.accumulate_aty(inst, d), z[p + "_g"]), p
+        assert core.dual_objective(inst, d) == pytest.approx(float(z[p + "_dual"]), rel=1e-13)
+
+
+def test_accumulate_aty_config2_duals_bitwise_oracle():
+    """At config-2 size (n = 1000, the GPU session's own duals after 8 passes)
+    the device accumulation equals the oracle's reference-order one."""
+    from oracle import oracle
+    inst = instances.config_instance(2)
+    sol = solver.solve(inst, SolverConfig(fixed_passes=8))
+    k, v = sol.duals.metric_arrays()
+    assert len(k) > 10000
+    g = core.accumulate_aty(inst, sol.duals)
+    ref = oracle.accumulate_aty_np(inst.n, k, v, sol.duals.pair_duals, inst.c_vector())
+    assert np.array_equal(g, ref)
+    # Dykstra invariant c + A'y = -eps W v (solver.py:256-281)
+    target = -inst.epsilon * np.concatenate([inst.reg_x * sol.state.xv, inst.reg_f * sol.state.fv])
+    assert np.max(np.abs(g - target)) <= 1e-9 * max(1.0, np.max(np.abs(target)))
+
+
+def test_accumulate_aty_edge_cases():
+    inst = instances.random_instance(5, seed=1)
+    d = core.DualStore(5, 1)                      # empty store: g = c exactly
+    assert np.array_equal(core.accumulate_aty(inst, d), inst.c_vector())
+    d.keys, d.vals = [np.array([((3 * 5 + 1) * 5 + 2) * 3], dtype=np.int64)], [np.array([1.0])]
+    from paper_1901_10084_b200 import _native
+    with pytest.raises(_native.NativeError) as ei:  # i > j: not a metric key
+        core.accumulate_aty(inst, d)
+    assert ei.value.code == _native.MP_ERR_ARG

@@ -2,11 +2,13 @@
 reference (tests/golden/make_golden.py).  CPU only."""
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
 from conftest import golden
+from oracle import oracle
 from paper_1901_10084_b200 import instances
 
 
@@ -165,3 +167,20 @@ def test_schedule_export_matches_python(oracle_lib):
         rounds = schedule.tiled_rounds(n, b)
         assert list(rn) == [len(r.units) for r in rounds]
         assert [tuple(t) for t in xz] == [(u.x, u.z) for r in rounds for u in r.units]
+
+
+def _aty_cases():
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "aty.npz"))
+    return z, [(p, int(z[p + "_n"])) for p in ("r", "c")]
+
+
+def test_oracle_accumulate_aty_matches_reference_golden():
+    """Both restatements of core.accumulate_aty (core.py:285-293) equal the
+    reference's own output bit for bit (tests/golden/make_aty_golden.py)."""
+    z, cases = _aty_cases()
+    for p, n in cases:
+        args = (n, z[p + "_keys"], z[p + "_vals"], z[p + "_pd"], z[p + "_c"])
+        g = oracle.accumulate_aty_np(*args)
+        assert np.array_equal(g, z[p + "_g"]), p
+        if p == "r":
+            assert np.array_equal(oracle.accumulate_aty_loop(*args), z[p + "_g"])
