@@ -137,6 +137,7 @@ struct TileArgs {
     const void *tmap;           // 2-D TMA descriptor of x (box wkp x BLK), null: element copies
     int32_t wkp;                // WK row pitch in doubles (>= b; the TMA box width)
     int32_t wrp;                // WR row pitch in doubles (>= W)
+    int32_t tma_store;          // interior WK blocks of the last band may be box-stored
 };
 
 #ifdef MP_TIMELINE
@@ -1582,11 +1583,12 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
 #endif
         const int slow = ts->pslow, fast = ts->pfast;
         if (slow > T.Lend) break;
-        bool busy = false;
+        bool busy = false, wk_elem = false;
         const int low_need = max(slow - T.ihi - T.z, T.jlo) / BLK;
         while (lo_res < low_need) {
             const bool st = last_band && wk_tma_store_ok(cc, lo_res);
             ring_block<W, false>(T, b, cc->wkp, cc->wrp, cc->ld, cc->x, WR, WK, lo_res, ptid, pn, r0, r1, last_band && !st);
+            wk_elem |= last_band && !st;
             if (st && ptid == 0) {
                 fence_proxy_async();  // the compute warps' (acquired) writes, to the async proxy
                 tma_store_2d(cc->tmap, T.klo, lo_res * BLK, smem_u32(WK + ((lo_res * BLK) & (W - 1)) * cc->wkp));
@@ -1599,6 +1601,10 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
 #endif
         const int need_fast = min(fast - T.ilo - T.klo, T.jhi) / BLK;
         const int want = min(need_fast + LOOKAHEAD, blast);
+        // A slot whose WK rows were just written back element by element (by
+        // every producer thread, rows split over warps) may be refilled by the
+        // loader thread's TMA box only after all of them have read it.
+        if (wk_elem && cc->tmap && hi_issued < want && hi_issued + 1 - lo_res < nres) producer_bar(pn);
         while (hi_issued < want && hi_issued + 1 - lo_res < nres) {
             ++hi_issued;
             ring_block<W, true>(T, b, cc->wkp, cc->wrp, cc->ld, cc->x, WR, WK, hi_issued, ptid, pn, r0, r1, cc->tmap == nullptr);
@@ -1845,7 +1851,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.rk_row_mul = (uint32_t)((0x100000000ull + 8ull * (unsigned)b - 1) / (8ull * (unsigned)b));
         cc.band_mul = (uint32_t)((65536u + (unsigned)RB - 1) / (unsigned)RB);
         cc.tmap = tmap;
-        cc.tma_st = T.z - T.klo + 1 == b;
+        cc.tma_st = a.tma_store && T.z - T.klo + 1 == b;
         cc.wkp = a.wkp;
         cc.wrp = a.wrp;
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0 && band < 8;

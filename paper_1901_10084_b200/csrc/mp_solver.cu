@@ -867,6 +867,7 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     ta.wkp = c.P;
     ta.wrp = c.PR;
     ta.tmap = x_tmap(h, c.P);
+    ta.tma_store = getenv("MP_NO_TMA_STORE") ? 0 : 1;
     return launch_tiles(h, c, ta, (int)cnt);
 }
 
