@@ -693,6 +693,9 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     const mp_handle::RoundCfg one = round_shape(h, 1);
     int cmax = MP_CMAX;
     if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(MP_CMAX, atoi(e)));
+    int fb = 2;  // cluster size for rounds whose clusters do not all fit at once
+    if (const char *e = getenv("MP_WAVE_C")) fb = atoi(e);
+    fb = std::min(fb, cmax);
     std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
     std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
     std::vector<bool> have(17, false);
@@ -700,6 +703,16 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     for (size_t r = 0; r < cnt_r.size(); ++r) {
         const int64_t cnt = cnt_r[r];
         mp_handle::RoundCfg best = one;
+        bool found = false;
+        if (const char *e = getenv("MP_FORCE_C")) {  // experiment: one C for every round, in waves if need be
+            const int C = std::max(1, std::min(MP_CMAX, atoi(e)));
+            if (C > 1 && (C - 1) * ((b + C - 1) / C) < b) {
+                if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
+                if (shape[C].S <= MAX_SLOTS && shape[C].smem <= 227 * 1024) best = shape[C];
+            }
+            h->rcfg.push_back(best);
+            continue;
+        }
         for (int C = std::min(cmax, b); C >= 2 && cnt > 0; --C) {
             const int RB = (b + C - 1) / C;
             if ((C - 1) * RB >= b || cnt * C > sms) continue;
@@ -709,8 +722,17 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
             if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
             if (cap[C] >= cnt) {
                 best = c;
+                found = true;
                 break;
             }
+        }
+        // More tiles than the device co-schedules as clusters: clusters of
+        // `fb` CTAs in waves beat one CTA per tile in a single wave (the
+        // longest tiles go first and set the round's time; configs 4 / 5:
+        // 0.68 -> 0.62 s and 4.8 -> 3.4 s per pass with C = 2 in waves).
+        if (!found && cnt > 0 && fb >= 2 && (fb - 1) * ((b + fb - 1) / fb) < b) {
+            if (!have[fb]) shape[fb] = round_shape(h, fb), have[fb] = true;
+            if (shape[fb].S <= MAX_SLOTS && shape[fb].smem <= 227 * 1024) best = shape[fb];
         }
         h->rcfg.push_back(best);
     }

@@ -14,8 +14,8 @@ are size-independent properties of the reference's algorithm --
 * the exported duals are valid reference keys (core.py:81-94) with theta > 0,
   and their count is the pass's nnz_metric.
 
-Config 5's biggest rounds hold more tiles than the GPU has SMs, so they run
-the one-CTA-per-tile kernel (S = 4) that no smaller config reaches.
+Config 5's biggest rounds hold more tiles than the GPU co-schedules, so they
+run as 2-CTA clusters in waves, which no smaller config reaches.
 """
 
 import os
@@ -106,7 +106,7 @@ def test_config4_full_size_sharded_and_resumed():
 
 
 def test_config5_full_size_sharded_and_resumed():
-    # n = 18000 Chung-Lu: the biggest rounds run one CTA per tile (S = 4)
+    # n = 18000 Chung-Lu: the biggest rounds run 2-CTA clusters in waves
     _sharded_and_resumed(5, passes=2, world=2)
 
 
@@ -115,12 +115,15 @@ def test_one_cta_tiles_long_rings_deterministic(monkeypatch):
     ~27 times, so a WK slot written back element by element is refilled by a
     TMA box many times per pass.  Regression for a missing producer barrier
     between the two (it showed as run-to-run differences at n >= 7000 only):
-    repeated runs and the element-copy staging must agree bit for bit."""
+    repeated runs and the element-copy staging must agree bit for bit -- and
+    so must clusters run in waves (MP_FORCE_C: 8-CTA clusters for every
+    round, 88 tiles x 8 CTAs in the biggest rounds) and the default plan."""
     import hashlib
     inst = instances.config_instance(4, n=7000)
     hashes = set()
-    for env in [{"MP_CLUSTER": "1"}, {"MP_CLUSTER": "1"}, {"MP_CLUSTER": "1", "MP_NO_TMA": "1"}]:
-        for k in ("MP_CLUSTER", "MP_NO_TMA"):
+    for env in [{"MP_CLUSTER": "1"}, {"MP_CLUSTER": "1"}, {"MP_CLUSTER": "1", "MP_NO_TMA": "1"},
+                {"MP_FORCE_C": "8"}, {}]:
+        for k in ("MP_CLUSTER", "MP_NO_TMA", "MP_FORCE_C"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
