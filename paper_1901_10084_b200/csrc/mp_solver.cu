@@ -350,6 +350,7 @@ struct mp_handle {
         size_t smem = 0;
     };
     std::vector<RoundCfg> rcfg;       // per round
+    int32_t tma_store = 1;            // box write-back of interior WK blocks (MP_NO_TMA_STORE: off)
     std::vector<int32_t> tile_round;  // round of each tile
     // schedule_kind "serial": the cube wavefront (mp_cube.cuh)
     std::vector<CubeDesc> cubes;          // all cubes, by cube level
@@ -889,7 +890,7 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     ta.wkp = c.P;
     ta.wrp = c.PR;
     ta.tmap = x_tmap(h, c.P);
-    ta.tma_store = getenv("MP_NO_TMA_STORE") ? 0 : 1;
+    ta.tma_store = h->tma_store;
     return launch_tiles(h, c, ta, (int)cnt);
 }
 
@@ -1252,6 +1253,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMemsetAsync(h->x, 0, dense, h->st));  // x = 0 (solver.py:112)
     TRY(cudaMalloc(&h->snap_x, dense));
     if ((rc = make_x_tmap(h))) return bail(rc);
+    h->tma_store = getenv("MP_NO_TMA_STORE") ? 0 : 1;
     tmark("x+tmap");
     TRY(cudaMalloc(&h->tmp, m * sizeof(double)));
     if ((rc = upload_packed(h, &h->d, inst->d_flat))) return bail(rc);
