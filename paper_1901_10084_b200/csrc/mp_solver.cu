@@ -697,6 +697,16 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     int fb = 2;  // cluster size for rounds whose clusters do not all fit at once
     if (const char *e = getenv("MP_WAVE_C")) fb = atoi(e);
     fb = std::min(fb, cmax);
+    // Rounds of up to minc_cnt tiles get at least minc CTAs per tile, in waves
+    // if need be: the longest tiles go first and their time is the round's
+    // time.  Measured (pass 3): config 3 (Chung-Lu, hub rows in the longest
+    // tiles) 167 -> 123 ms; config 4 (uniform) 586 -> 590 ms; config 5 -1%.
+    // Larger rounds are throughput-bound and keep the largest fitting C.
+    int minc = 6;
+    if (const char *e = getenv("MP_MIN_C")) minc = atoi(e);
+    minc = std::min(minc, cmax);
+    int64_t minc_cnt = 50;
+    if (const char *e = getenv("MP_MIN_C_CNT")) minc_cnt = atoll(e);
     std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
     std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
     std::vector<bool> have(17, false);
@@ -727,11 +737,16 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
                 break;
             }
         }
+        // small rounds: at least minc CTAs per tile (see minc above)
+        if (best.C < minc && cnt > 0 && cnt <= minc_cnt && (minc - 1) * ((b + minc - 1) / minc) < b) {
+            if (!have[minc]) shape[minc] = round_shape(h, minc), have[minc] = true;
+            if (shape[minc].S <= MAX_SLOTS && shape[minc].smem <= 227 * 1024) best = shape[minc];
+        }
         // More tiles than the device co-schedules as clusters: clusters of
         // `fb` CTAs in waves beat one CTA per tile in a single wave (the
         // longest tiles go first and set the round's time; configs 4 / 5:
         // 0.68 -> 0.62 s and 4.8 -> 3.4 s per pass with C = 2 in waves).
-        if (!found && cnt > 0 && fb >= 2 && (fb - 1) * ((b + fb - 1) / fb) < b) {
+        if (!found && best.C == 1 && cnt > 0 && fb >= 2 && (fb - 1) * ((b + fb - 1) / fb) < b) {
             if (!have[fb]) shape[fb] = round_shape(h, fb), have[fb] = true;
             if (shape[fb].S <= MAX_SLOTS && shape[fb].smem <= 227 * 1024) best = shape[fb];
         }
