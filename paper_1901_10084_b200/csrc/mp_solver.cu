@@ -700,12 +700,12 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     // Rounds of up to minc_cnt tiles get at least minc CTAs per tile, in waves
     // if need be: the longest tiles go first and their time is the round's
     // time.  Measured (pass 3): config 3 (Chung-Lu, hub rows in the longest
-    // tiles) 167 -> 123 ms; config 4 (uniform) 586 -> 590 ms; config 5 -1%.
+    // tiles) 167 -> 123 ms; config 4 (uniform) 586 -> 592 ms; config 5 -1%.
     // Larger rounds are throughput-bound and keep the largest fitting C.
     int minc = 6;
     if (const char *e = getenv("MP_MIN_C")) minc = atoi(e);
     minc = std::min(minc, cmax);
-    int64_t minc_cnt = 50;
+    int64_t minc_cnt = sms * 3 / 8;  // 55 on B200 (50: config 3 128 ms, 55: 123 ms, 64: config 4 +1.4%)
     if (const char *e = getenv("MP_MIN_C_CNT")) minc_cnt = atoll(e);
     std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
     std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
