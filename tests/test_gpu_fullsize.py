@@ -133,3 +133,30 @@ def test_one_cta_tiles_long_rings_deterministic(monkeypatch):
         hashes.add(hashlib.sha1(x.tobytes() + f.tobytes()).hexdigest())
         s.close()
     assert len(hashes) == 1
+
+
+@pytest.mark.parametrize("env", [{"MP_FORCE_C": "8"}, {"MP_FORCE_C": "2"}, {}])
+def test_cluster_waves_bitwise_oracle(oracle_lib, monkeypatch, env):
+    """Clusters in waves (more tiles in a round than the device co-schedules
+    as clusters: n = 1400 has rounds of 17 tiles, 8-CTA clusters fit 15 at a
+    time) against the oracle, bit for bit, on a Chung-Lu instance (hub rows)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inst = instances.config_instance(3, n=1400)
+    sess = DeviceSession(inst, "tiled", B)
+    ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=B,
+                                  workers=os.cpu_count() or 1)
+    for _ in range(4):
+        st = sess.run(1)[0]
+        rs = ref.run_pass()
+        assert st.max_violation == rs.max_violation
+    x, f = sess.state()
+    rx, rf = ref.state()
+    assert np.array_equal(x, rx) and np.array_equal(f, rf)
+    keys, vals, _ = sess.duals()
+    rk, rv = ref.duals()
+    assert len(keys) > 0
+    o1, o2 = np.argsort(keys), np.argsort(rk)
+    assert np.array_equal(keys[o1], rk[o2]) and np.array_equal(vals[o1], rv[o2])
+    ref.close()
+    sess.close()
