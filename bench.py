@@ -1,9 +1,11 @@
 #!/usr/bin/env python3
 """Benchmark: triangle projections/sec of the Dykstra sweep (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--tile-b 40]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--tile-b 40]
     python bench.py --impl reference ...        # CPU reference arm (oracle port)
 
+Default workload: BASELINE config 3 (n = 4000 Chung-Lu), the largest config
+BASELINE.json assigns to one GPU.
 A "step" is one full Dykstra pass (all 3*C(n,3) metric rows in the paper's
 tiled order + the pair phase) over the config's seeded synthetic instance.
 ``value`` = K * 3*C(n,3) * N / t with t the device time (CUDA events on the
@@ -11,8 +13,9 @@ library's stream) of the K timed passes, max over ranks; L2 is flushed
 (256 MiB write) before every timed pass.  ``e2e`` is the same metric through
 the public ``solve()`` API from host arrays (instance upload, every pass,
 per-pass stats and the final x/f/duals download inside the wall-clock).
-Multi-GPU (torchrun) runs independent replicas, one per GPU (weak scaling);
-`--sharded` runs one instance over all ranks instead (strong scaling).
+Multi-GPU (torchrun) defaults to BASELINE config 4 (n = 10000) sharded over
+all ranks (one instance, strong scaling); an explicit --config
+without --sharded runs independent replicas, one per GPU (weak scaling).
 """
 
 from __future__ import annotations
@@ -183,9 +186,42 @@ def list_index(spec):
     return 0
 
 
-def cpu_sample(inst, b, passes_warm, passes_timed, threads):
+def cpu_info():
+    """CPU model and core counts of the host (reported beside every CPU rate)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except ImportError:
+        phys = None
+    return {"cpu_model": model, "physical_cores": phys, "logical_cpus": os.cpu_count()}
+
+
+def p1_round_limit(n, b, target_rows):
+    """Smallest prefix of the tiled rounds holding >= target_rows metric rows."""
+    from paper_1901_10084_b200 import schedule
+    acc = 0
+    for r, rnd in enumerate(schedule.tiled_rounds(n, b)):
+        acc += 3 * rnd.size
+        if acc >= target_rows:
+            return r + 1, acc
+    return 0, acc
+
+
+def cpu_sample(inst, b, passes_warm, passes_timed, threads, p1_rows=0):
     """Time the CPU oracle (a C port of the reference kernels, threaded like
-    the reference's worker pool) on a bounded sample of the workload."""
+    the reference's worker pool) on a bounded sample of the workload.
+    With ``p1_rows`` also a single-thread (P = 1) rate over the first rounds
+    of the next pass, started from the warmed x/f (no stored duals: the CPU
+    cost is the row visits, exact steps are < 0.1% of them)."""
     from oracle import oracle
     oracle.build()
     o = oracle.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=b, workers=threads)
@@ -195,29 +231,49 @@ def cpu_sample(inst, b, passes_warm, passes_timed, threads):
     for _ in range(passes_timed):
         o.run_pass()
     dt = time.perf_counter() - t0
+    p1 = None
+    if p1_rows:
+        limit, _ = p1_round_limit(inst.n, b, p1_rows)
+        x, f = o.state()
+        o1 = oracle.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=b, workers=1)
+        o1.set_state(x, f)
+        rows, t1 = o1.timed_rounds(limit)
+        o1.close()
+        p1 = {"value": rows / t1, "unit": UNIT, "cores": 1,
+              "sample": f"first {limit} rounds of pass {passes_warm + passes_timed + 1} "
+                        f"({rows:.3e} metric rows, {t1:.1f} s) from the warmed x/f, 1 thread"}
     o.close()
-    return passes_timed * rows_per_pass(inst.n) / dt, dt
+    return passes_timed * rows_per_pass(inst.n) / dt, dt, p1
 
 
 def run_reference(args):
+    """Reference arm: the CPU oracle (C port of the reference's numba kernels,
+    threaded like its worker pool) on all host threads.  A bounded sample so
+    the run ends in minutes at config 3: min(W, 1) warm-up passes, then
+    min(K, 3) timed full passes."""
     ws, rank, _ = dist_env()
     if ws > 1 and rank != 0:
         return 0
     from paper_1901_10084_b200 import instances
-    spec = instances.CONFIGS[args.config]
-    inst = instances.config_instance(args.config)
+    cfg = args.config or 3
+    spec = instances.CONFIGS[cfg]
+    inst = instances.config_instance(cfg)
     threads = args.cpu_threads or os.cpu_count() or 1
-    rate, dt = cpu_sample(inst, args.tile_b, args.warmup, args.steps, threads)
+    warm = min(args.warmup, 1) if inst.n > 1500 else args.warmup
+    timed = min(args.steps, 3) if inst.n > 1500 else args.steps
+    rate, dt, _ = cpu_sample(inst, args.tile_b, warm, timed, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": args.gpus, "steps": timed, "warmup": warm,
+        "ms_per_step": dt / timed * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
         "config": {"workload": workload_name(spec, args.tile_b), "n": inst.n, "tile_b": args.tile_b,
                    "parallelism": f"{threads} CPU threads"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"passes {args.warmup + 1}..{args.warmup + args.steps} of the "
-                                   f"config (after {args.warmup} warm-up passes), oracle/ C port "
+                         **cpu_info(),
+                         "sample": f"passes {warm + 1}..{warm + timed} of the config (after {warm} "
+                                   f"warm-up passes; requested --steps {args.steps} --warmup "
+                                   f"{args.warmup}, capped to bound the CPU run), oracle/ C port "
                                    "of _kernels.metric_units_pass + pair_pass"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -235,6 +291,9 @@ def run_gpu(args):
     from paper_1901_10084_b200 import instances, schedule
     from paper_1901_10084_b200.solver import DeviceSession, SolverConfig, solve
 
+    if not args.config:  # defaults: config 3 on one GPU, config 4 sharded over N > 1
+        args.config = 4 if ws > 1 else 3
+        args.sharded = args.sharded or ws > 1
     spec = instances.CONFIGS[args.config]
     inst = instances.config_instance(args.config)
     n, b = inst.n, args.tile_b
@@ -279,6 +338,9 @@ def run_gpu(args):
     metric_bytes = args.steps * 16 * tx + 12 * nnz_io  # x read+write per touched pair, 12 B/dual
     achieved = metric_bytes / (metric_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
+    if args.sharded:  # metric_bytes covers the whole instance: compare with the whole box
+        peak *= ws
+        peak_src += f" x {ws} GPUs"
     n_rounds = sum(1 for r in schedule.tiled_rounds(n, b) if r.units)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config, b),
@@ -289,6 +351,11 @@ def run_gpu(args):
                 "launches_per_pass": n_rounds + 2,
                 "critical_levels_per_pass": schedule.critical_levels(n, b),
                 "ns_per_level": metric_ms * 1e6 / args.steps / schedule.critical_levels(n, b)}
+    # whole pass (SURVEY 8(d) B_pass): + 72 B per pair for the pair phase
+    pass_bytes = metric_bytes + args.steps * 72 * (n * (n - 1) // 2)
+    roofline["whole_pass"] = {"bytes_per_pass": pass_bytes / args.steps,
+                              "achieved": pass_bytes / t_dev / 1e9,
+                              "frac": pass_bytes / t_dev / 1e9 / peak}
 
     # ---- end to end through the public API (host buffers) ---------------------
     total = args.warmup + args.steps
@@ -327,11 +394,12 @@ def run_gpu(args):
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = args.cpu_threads or os.cpu_count() or 1
         warm, timed = (2, 3) if n <= 1500 else (1, 1)
-        rate, dt = cpu_sample(inst, b, warm, timed, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+        rate, dt, p1 = cpu_sample(inst, b, warm, timed, threads, p1_rows=2.0e9 if n > 1500 else 2.0e8)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", **cpu_info(),
                "sample": f"passes {warm + 1}..{warm + timed} of the same instance after {warm} "
                          f"warm-up passes ({dt:.1f} s), oracle/ C port of the reference kernels, "
-                         f"{threads} threads"}
+                         f"{threads} threads",
+               "p1": p1}
 
     if rank == 0:
         line = {
@@ -361,7 +429,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=0,
+                    help="BASELINE config (default 3: the largest one-GPU config; "
+                         "4 sharded under torchrun)")
     ap.add_argument("--tile-b", type=int, default=40)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-threads", type=int, default=0)

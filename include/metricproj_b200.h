@@ -187,6 +187,19 @@ int mp_max_violation(int64_t n, const double *xv, const double *fv, const double
 int mp_accumulate_aty(int64_t n, int64_t nnz, const int64_t *keys, const double *vals,
                       const double *pair_duals, const double *c, double *g);
 
+/* Kernel-level drop-in for projection.dykstra_step(state, key, y_old, instance)
+ * (projection.py:63-87), batched: rows r = 0..nrows-1 are applied in order to
+ * the value vector v[nv] (host buffer, updated in place).  Row r has nent[r]
+ * entries (3 metric, 2 pair): positions pos[3r+e] into v, coefficients
+ * coef[3r+e] (+-1, core._row_entries), weights reg[3r+e] (reg_x or reg_f of
+ * the entry), right-hand side rhs[r] and old dual y_old[r] >= 0 (negative ->
+ * MP_ERR_ARG, the reference's ValueError).  theta[r] receives theta_plus
+ * (0 when <= THETA_FLOOR), changed[r] whether any entry moved.  Runs on the
+ * current CUDA device, in dykstra_step's own association. */
+int mp_dykstra_steps(int64_t nrows, const int32_t *nent, const int64_t *pos, const double *coef,
+                     const double *reg, const double *rhs, const double *y_old, double eps,
+                     int64_t nv, double *v, double *theta, int32_t *changed);
+
 /* Correlation-clustering instance of a graph (instance.cc_instance,
  * instance.py:124-161): closed-neighbourhood Jaccard J of every pair (the
  * sparse product B*B^T on the device), s = log((1 + J - guard) / (1 - J +

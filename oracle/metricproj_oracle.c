@@ -136,6 +136,7 @@ typedef struct mpo_solver {
     /* per-pass worker results */
     double *wviol;
     int64_t *wsteps;
+    int64_t round_limit; /* timing samples only: 0 = whole pass */
 } mpo_solver;
 
 /* One Dykstra step of a metric row; the three x positions and their W^-1
@@ -256,7 +257,9 @@ static void *worker_main(void *arg) {
                     steps += 3;
                 }
     } else {
-        for (int64_t r = 0; r < S->sched.nrounds; ++r) {
+        const int64_t nr = S->round_limit > 0 && S->round_limit < S->sched.nrounds
+                               ? S->round_limit : S->sched.nrounds;
+        for (int64_t r = 0; r < nr; ++r) {
             const mpo_round *R = &S->sched.rounds[r];
             for (int64_t pos = 0; pos < R->ntiles; ++pos) {
                 if ((pos + 1) % p != w) continue;
@@ -268,7 +271,7 @@ static void *worker_main(void *arg) {
     }
     int64_t lo = (int64_t)w * S->m / p, hi = (int64_t)(w + 1) * S->m / p;
     double pv = 0.0;
-    steps += pair_range(S, lo, hi, &pv);
+    if (S->round_limit <= 0) steps += pair_range(S, lo, hi, &pv);
     if (pv > viol) viol = pv;
     S->wviol[w] = viol;
     S->wsteps[w] = steps;
@@ -400,6 +403,12 @@ double mpo_run_pass(mpo_solver *S, int64_t *steps) {
     if (steps) *steps = st;
     return viol;
 }
+
+/* Timing samples only (bench.py's P = 1 CPU row): later passes stop after the
+ * first `limit` rounds of the tiled/diagonal schedule and skip the pair
+ * phase, so `steps` counts exactly the metric rows visited.  0 restores
+ * whole passes.  A limited pass leaves the solver mid-pass: not a result. */
+void mpo_set_round_limit(mpo_solver *S, int64_t limit) { S->round_limit = limit; }
 
 /* Exact violation scan (_kernels.py:28-57). */
 double mpo_max_violation(const double *xv, const double *fv, const double *dflat, int64_t n) {

@@ -69,6 +69,7 @@ def lib():
         L.mpo_num_tiles.restype = ctypes.c_int64
         L.mpo_num_tiles.argtypes = [P]
         L.mpo_get_schedule.argtypes = [P, I, I]
+        L.mpo_set_round_limit.argtypes = [P, ctypes.c_int64]
         _lib = L
     return _lib
 
@@ -159,6 +160,20 @@ class OracleSolver:
         xz = np.empty((nt, 2), dtype=np.int64)
         L.mpo_get_schedule(self._h, _ip(rn), _ip(xz))
         return rn, xz
+
+    def timed_rounds(self, limit):
+        """Timing sample only (bench.py's P = 1 row): run the first ``limit``
+        rounds of one pass (no pair phase) and return (metric rows visited,
+        seconds).  The solver is left mid-pass; close it afterwards."""
+        import time
+        L = lib()
+        L.mpo_set_round_limit(self._h, int(limit))
+        steps = ctypes.c_int64(0)
+        t0 = time.perf_counter()
+        L.mpo_run_pass(self._h, ctypes.byref(steps))
+        dt = time.perf_counter() - t0
+        L.mpo_set_round_limit(self._h, 0)
+        return steps.value, dt
 
     def run_pass(self):
         steps = ctypes.c_int64(0)
@@ -307,6 +322,36 @@ def py_pass(n, eps, x, f, d_flat, winvx, winvf, duals, pair_duals, kind="tiled",
                 f[p] -= coef * winvf[p]
             pair_duals[p, row] = theta if theta > THETA_FLOOR else 0.0
     return viol, new
+
+
+def dykstra_step_py(xv, fv, reg_x, reg_f, eps, n, kind, i, j, k, y_old, d_flat):
+    """One row step in projection.dykstra_step's own association
+    (projection.py:63-87): sums over the row's entries from 0, b last,
+    W^-1 = 1/reg per entry.  Updates xv/fv in place; returns (theta, changed)."""
+    m = pair_count(n)
+    if kind <= 2:
+        pij, pik, pjk = _pos(n, i, j), _pos(n, i, k), _pos(n, j, k)
+        plus, m1, m2 = ((pij, pik, pjk), (pik, pij, pjk), (pjk, pij, pik))[kind]
+        ent = ((plus, 1.0), (m1, -1.0), (m2, -1.0))
+        b = 0.0
+    else:
+        p = _pos(n, i, j)
+        ent = ((p, 1.0 if kind == 3 else -1.0), (m + p, -1.0))
+        b = float(d_flat[p]) if kind == 3 else -float(d_flat[p])
+    vals = [xv[q] if q < m else fv[q - m] for q, _ in ent]
+    winv = [1.0 / (reg_x[q] if q < m else reg_f[q - m]) for q, _ in ent]
+    d0 = sum(c * v for (_, c), v in zip(ent, vals)) - b
+    s = sum(c * c * w for (_, c), w in zip(ent, winv))
+    delta = d0 + y_old * s / eps
+    theta = eps * delta / s if delta > 0.0 else 0.0
+    coef = (y_old - theta) / eps
+    if coef != 0.0:
+        for (q, c), w in zip(ent, winv):
+            if q < m:
+                xv[q] += coef * c * w
+            else:
+                fv[q - m] += coef * c * w
+    return (0.0 if theta <= THETA_FLOOR else theta), coef != 0.0
 
 
 # ---------------------------------------------------------------------------

@@ -96,7 +96,8 @@ EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dua
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
            "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_check_division",
            "mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
-           "mp_group_run_passes", "mp_cc_instance", "mp_accumulate_aty", "mp_last_error", "mp_version")
+           "mp_group_run_passes", "mp_cc_instance", "mp_accumulate_aty", "mp_dykstra_steps",
+           "mp_last_error", "mp_version")
 
 _lib = None
 
@@ -160,8 +161,11 @@ def load():
                                       ctypes.POINTER(MPPassStats)]
     L.mp_cc_instance.argtypes = [ctypes.c_int64, I, ctypes.POINTER(ctypes.c_int32), ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, D, D]
+    L.mp_dykstra_steps.argtypes = [ctypes.c_int64, ctypes.POINTER(ctypes.c_int32), I, D, D, D, D,
+                                   ctypes.c_double, ctypes.c_int64, D, D,
+                                   ctypes.POINTER(ctypes.c_int32)]
     for name in ("mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
-                 "mp_group_run_passes", "mp_cc_instance"):
+                 "mp_group_run_passes", "mp_cc_instance", "mp_dykstra_steps"):
         getattr(L, name).restype = ctypes.c_int
     L.mp_last_error.restype = ctypes.c_char_p
     L.mp_version.restype = ctypes.c_char_p

@@ -365,4 +365,44 @@ __global__ void cc_map_kernel(const uint32_t *inter, const int64_t *rowptr, int6
     }
 }
 
+// ---------------------------------------------------------------------------
+// projection.dykstra_step (projection.py:63-87): single constraint rows applied
+// in order by one thread, in that function's own association -- the sums over
+// the row's entries start from 0 and b is subtracted last (for the lower pair
+// row that is ((0 - x) - f) - (-d), not the sweep kernel's (d - x) - f), and
+// W^-1 is formed as 1/reg per entry.
+// ---------------------------------------------------------------------------
+struct StepRow {
+    int32_t nent, pad;   // 2 (pair row) or 3 (metric row)
+    int64_t pos[3];      // positions in the value vector
+    double coef[3];      // +-1 (core._row_entries)
+    double reg[3];       // reg_x / reg_f of each entry
+    double rhs;          // b of the row (0 metric, +d upper, -d lower)
+    double y;            // old dual, >= 0
+};
+
+__global__ void single_steps_kernel(const StepRow *rows, int64_t nrows, double eps, double *v,
+                                    double *theta_out, int32_t *changed_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int64_t r = 0; r < nrows; ++r) {
+        const StepRow R = rows[r];
+        double winv[3], acc = 0.0, s = 0.0;
+        for (int e = 0; e < R.nent; ++e) {
+            winv[e] = __ddiv_rn(1.0, R.reg[e]);
+            acc = __dadd_rn(acc, __dmul_rn(R.coef[e], v[R.pos[e]]));
+        }
+        const double d0 = __dsub_rn(acc, R.rhs);
+        for (int e = 0; e < R.nent; ++e)
+            s = __dadd_rn(s, __dmul_rn(__dmul_rn(R.coef[e], R.coef[e]), winv[e]));
+        const double delta = __dadd_rn(d0, __ddiv_rn(__dmul_rn(R.y, s), eps));
+        double theta = delta > 0.0 ? __ddiv_rn(__dmul_rn(eps, delta), s) : 0.0;
+        const double coef = __ddiv_rn(__dsub_rn(R.y, theta), eps);
+        if (coef != 0.0)
+            for (int e = 0; e < R.nent; ++e)
+                v[R.pos[e]] = __dadd_rn(v[R.pos[e]], __dmul_rn(__dmul_rn(coef, R.coef[e]), winv[e]));
+        theta_out[r] = theta <= THETA_FLOOR ? 0.0 : theta;
+        changed_out[r] = coef != 0.0;
+    }
+}
+
 }  // namespace mp

@@ -2083,6 +2083,70 @@ int mp_max_violation(int64_t n, const double *xv, const double *fv, const double
     return MP_OK;
 }
 
+int mp_dykstra_steps(int64_t nrows, const int32_t *nent, const int64_t *pos, const double *coef,
+                     const double *reg, const double *rhs, const double *y_old, double eps,
+                     int64_t nv, double *v, double *theta, int32_t *changed) {
+    g_err.clear();
+    if (nrows < 0 || nv < 0 || (nrows > 0 && (!nent || !pos || !coef || !reg || !rhs || !y_old ||
+                                              !v || !theta || !changed)))
+        return fail(MP_ERR_ARG, "bad argument");
+    if (!(eps > 0.0)) return fail(MP_ERR_ARG, "epsilon must be positive, got %g", eps);
+    if (nrows == 0) return MP_OK;
+    std::vector<StepRow> rows((size_t)nrows);
+    for (int64_t r = 0; r < nrows; ++r) {
+        if (nent[r] != 2 && nent[r] != 3) return fail(MP_ERR_ARG, "row %lld: %d entries", (long long)r, nent[r]);
+        if (!(y_old[r] >= 0.0))
+            return fail(MP_ERR_ARG, "dual values are nonnegative, got %g", y_old[r]);
+        StepRow &R = rows[(size_t)r];
+        R.nent = nent[r];
+        R.pad = 0;
+        for (int e = 0; e < 3; ++e) {
+            const bool on = e < nent[r];
+            R.pos[e] = on ? pos[3 * r + e] : 0;
+            R.coef[e] = on ? coef[3 * r + e] : 0.0;
+            R.reg[e] = on ? reg[3 * r + e] : 1.0;
+            if (on && (R.pos[e] < 0 || R.pos[e] >= nv))
+                return fail(MP_ERR_ARG, "row %lld: position out of range", (long long)r);
+        }
+        R.rhs = rhs[r];
+        R.y = y_old[r];
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MP_ERR_CUDA, "no CUDA device available; there is no CPU fallback");
+    StepRow *drows = nullptr;
+    double *dv = nullptr, *dth = nullptr;
+    int32_t *dch = nullptr;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    auto cleanup = [&]() {
+        cudaFree(drows);
+        cudaFree(dv);
+        cudaFree(dth);
+        cudaFree(dch);
+        cudaStreamDestroy(st);
+    };
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc(&drows, rows.size() * sizeof(StepRow))) != cudaSuccess ||
+        (e = cudaMalloc(&dv, (size_t)std::max<int64_t>(nv, 1) * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dth, (size_t)nrows * sizeof(double))) != cudaSuccess ||
+        (e = cudaMalloc(&dch, (size_t)nrows * sizeof(int32_t))) != cudaSuccess) {
+        cleanup();
+        return fail(MP_ERR_OOM, "cudaMalloc: %s", cudaGetErrorString(e));
+    }
+    cudaMemcpyAsync(drows, rows.data(), rows.size() * sizeof(StepRow), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dv, v, (size_t)nv * sizeof(double), cudaMemcpyHostToDevice, st);
+    single_steps_kernel<<<1, 32, 0, st>>>(drows, nrows, eps, dv, dth, dch);
+    cudaMemcpyAsync(v, dv, (size_t)nv * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(theta, dth, (size_t)nrows * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(changed, dch, (size_t)nrows * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cleanup();
+    if (e != cudaSuccess) return fail(MP_ERR_CUDA, "dykstra_steps: %s", cudaGetErrorString(e));
+    return MP_OK;
+}
+
 int mp_accumulate_aty(int64_t n, int64_t nnz, const int64_t *keys, const double *vals,
                       const double *pair_duals, const double *c, double *g) {
     g_err.clear();

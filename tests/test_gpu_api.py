@@ -204,3 +204,35 @@ def test_accumulate_aty_edge_cases():
     with pytest.raises(_native.NativeError) as ei:  # i > j: not a metric key
         core.accumulate_aty(inst, d)
     assert ei.value.code == _native.MP_ERR_ARG
+
+
+def test_dykstra_step_bitwise_reference_golden():
+    """projection.dykstra_step (projection.py:63-87) on the device through
+    mp_dykstra_steps: the reference's own single-row steps (tests/golden/
+    steps.npz: all five kinds, general W, y_old = 0 and > 0, applied in
+    sequence) bit for bit, plus the worked example and the y_old < 0 error."""
+    import paper_1901_10084_b200 as mp
+    from conftest import golden
+    g = golden("steps")
+    for c in range(6):
+        n, eps = int(g[f"c{c}_n"]), float(g[f"c{c}_eps"])
+        m = n * (n - 1) // 2
+        inst = core.ProblemInstance(n, g[f"c{c}_D"], np.ones((n, n)) - np.eye(n), epsilon=eps,
+                                    reg_x=g[f"c{c}_regx"].copy(), reg_f=g[f"c{c}_regf"].copy())
+        st = core.PrimalState(n, g[f"c{c}_x0"].copy(), g[f"c{c}_f0"].copy())
+        for t, (kind, i, j, k) in enumerate(g[f"c{c}_keys"]):
+            key = core.ConstraintKey(core.Kind(int(kind)), int(i), int(j), int(k))
+            o = mp.dykstra_step(st, key, float(g[f"c{c}_y"][t]), inst)
+            assert isinstance(o, mp.StepOutcome)
+            assert o.theta_plus == g[f"c{c}_theta"][t] and o.changed == bool(g[f"c{c}_changed"][t])
+        assert np.array_equal(st.xv, g[f"c{c}_x1"]) and np.array_equal(st.fv, g[f"c{c}_f1"]), c
+        assert len(st.xv) == m
+    # worked example (reference tests/test_acceptance.py:86-98)
+    inst3 = core.ProblemInstance(3, np.zeros((3, 3)), np.ones((3, 3)) - np.eye(3), epsilon=0.7)
+    st3 = core.PrimalState(3)
+    st3.set_x(0, 1, 1.0)
+    o = mp.dykstra_step(st3, core.ConstraintKey(core.Kind.METRIC_IJ, 0, 1, 2), 0.0, inst3)
+    sg = golden("small_cases")
+    assert np.array_equal(st3.xv, sg["worked_x"]) and o.theta_plus == float(sg["worked_theta"])
+    with pytest.raises(ValueError):
+        mp.dykstra_step(st3, core.ConstraintKey(core.Kind.METRIC_IJ, 0, 1, 2), -1.0, inst3)
