@@ -140,6 +140,14 @@ struct TileArgs {
     int32_t tma_store;          // interior WK blocks of the last band may be box-stored
 };
 
+#ifdef MP_TILETIME
+// Diagnostic per-tile timing (tools/tile_times.py): per (round, tile, band)
+// 16 u64 slots: globaltimer at kernel start / after the prologue / after the
+// sweep / at the end, then the sweep's cycle counters summed over the
+// compute warps (TR_PRED_WAIT .. TR_COLD_CALLS order, see TraceSlot).
+constexpr int TT_ROUNDS = 256, TT_TILES = 128, TT_BANDS = 8, TT_REC = 16;
+constexpr size_t TT_SLOTS = (size_t)TT_ROUNDS * TT_TILES * TT_BANDS * TT_REC;
+#endif
 #ifdef MP_TIMELINE
 // Diagnostic timeline (tools/timeline.py): per (band, warp, batch) the clock64
 // values [wait start, work start, work end, cold flag, levels replayed, lookup,
@@ -148,6 +156,8 @@ struct TileArgs {
 constexpr int TL_MAXB = 512;
 constexpr int TL_REC = 8;  // u64 per batch record
 constexpr int TL_SLOTS = 8 * 16 * TL_MAXB * TL_REC;
+#endif
+#if defined(MP_TIMELINE) || defined(MP_TILETIME)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -204,6 +214,7 @@ struct CtaConst {
     int32_t tma_st;       // the tile's K is b wide: interior WK blocks are stored by TMA
     int32_t wkp;          // WK row pitch (doubles)
     int32_t wrp;          // WR row pitch (doubles)
+    unsigned long long *tt;  // MP_TILETIME builds: this CTA's record, else null
 };
 
 #ifndef MP_CMAX  // largest cluster (CTAs per tile) the host plans; > 8 is non-portable
@@ -1351,7 +1362,9 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
     // alias-free levels: x_ik is this thread's alone and lives in a register,
     // loaded once the first batch's dependencies are met (the previous
     // phase's last level may still write it in the predecessor warp)
-#ifdef MP_TRACE
+#if defined(MP_TILETIME)
+    const bool tr = cc.tt != nullptr;
+#elif defined(MP_TRACE)
     const bool tr = cc.trace != nullptr;
 #else
     constexpr bool tr = false;  // build with -DMP_TRACE for mp_trace counters
@@ -1492,6 +1505,18 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
         L = Le + 1;
         if (tr) { t1 = clock64(); c_rel += t1 - t0; t0 = t1; }
     }
+#ifdef MP_TILETIME
+    if (tr && lane == 0) {
+        atomicAdd(&cc.tt[4 + TR_PRED_WAIT], c_pred);
+        atomicAdd(&cc.tt[4 + TR_RING_WAIT], c_ring);
+        atomicAdd(&cc.tt[4 + TR_HOT], c_hot);
+        atomicAdd(&cc.tt[4 + TR_COLD], c_cold);
+        atomicAdd(&cc.tt[4 + TR_RELEASE], c_rel);
+        atomicAdd(&cc.tt[4 + TR_LEVELS], (unsigned long long)(Lb - La + 1));
+        atomicAdd(&cc.tt[4 + TR_COLD_CALLS], n_cold);
+    }
+    return;
+#endif
     if (tr && lane == 0) {
         atomicAdd(&cc.trace[TR_PRED_WAIT], c_pred);
         atomicAdd(&cc.trace[TR_RING_WAIT], c_ring);
@@ -1858,6 +1883,11 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.B32 = B32;
         cc.lw = a.lw;
         cc.colm = a.colm;
+        cc.tt = nullptr;
+#ifdef MP_TILETIME
+        if (a.trace && a.round_id < TT_ROUNDS && blockIdx.x / C < TT_TILES && band < TT_BANDS)
+            cc.tt = a.trace + (((size_t)a.round_id * TT_TILES + blockIdx.x / C) * TT_BANDS + band) * TT_REC;
+#endif
     }
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
     if (tid < 32) ts.done[tid] = T.Lbeg - 1;
@@ -1866,6 +1896,16 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     // arguments; x, the dual pools and the counters were written by the
     // previous round, so wait for it here.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef MP_TILETIME
+    __syncthreads();
+    if (tid == 0 && cc.tt) {
+        cc.tt[0] = gtimer();
+        cc.tt[12] = (unsigned long long)(T.ilo + 1);  // 0 = no record
+        cc.tt[13] = (unsigned long long)T.z;
+        cc.tt[14] = (unsigned long long)C;
+        cc.tt[15] = (unsigned long long)nwc;
+    }
+#endif
 
     // --- staging prologue (all threads) -----------------------------------
     rk_block<true>(T, b, a.ld, a.x, RK, tid, nt, 0, b);
@@ -1897,6 +1937,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     // no CTA may forward into (or publish to) a CTA before its staging landed
     if (C > 1) cluster_sync_all();
     const long long tk1 = clock64();
+#ifdef MP_TILETIME
+    if (tid == 0 && cc.tt) cc.tt[1] = gtimer();
+#endif
 
     double viol = 0.0;
     if (warp >= nwc) {
@@ -1948,6 +1991,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     }
 #endif
     const long long tk2 = clock64();
+#ifdef MP_TILETIME
+    if (tid == 0 && cc.tt) cc.tt[2] = gtimer();
+#endif
     // own WR and RK rows (a row's final values live in its band); the last
     // band holds the final WK (every band forwards its WK writes downstream)
     for (int bk = ts.lo_res; bk <= ts.hi_issued; ++bk) {
@@ -1977,6 +2023,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
     }
     if (C > 1) cluster_sync_all();  // late remote stores must not hit an exited CTA
+#ifdef MP_TILETIME
+    if (tid == 0 && cc.tt) cc.tt[3] = gtimer();
+#endif
 }
 
 // dynamic shared memory of one CTA

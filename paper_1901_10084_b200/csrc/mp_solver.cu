@@ -1758,7 +1758,9 @@ int mp_trace(mp_handle *h, int32_t enable, uint64_t *out, int32_t nslots) {
     g_err.clear();
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
-#ifdef MP_TIMELINE
+#if defined(MP_TILETIME)
+    const size_t ns = TT_SLOTS;  // diagnostic build: per-tile times
+#elif defined(MP_TIMELINE)
     const size_t ns = TL_SLOTS;  // diagnostic build: the per-batch timeline
 #else
     const size_t ns = TR_NSLOTS;

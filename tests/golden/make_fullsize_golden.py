@@ -128,7 +128,7 @@ def run_oracle(config, passes, workers=None):
     from oracle import oracle
     oracle.build()
     inst = instances.config_instance(config)
-    workers = workers or os.cpu_count() or 1
+    workers = workers or int(os.environ.get("MP_GOLDEN_THREADS", 0)) or os.cpu_count() or 1
     ref = oracle.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=B,
                               workers=workers)
     rec = new_rec()

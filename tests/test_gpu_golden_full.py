@@ -10,7 +10,8 @@ pass by pass, bit for bit (tests/golden/make_fullsize_golden.py).
 Per pass: sha256 of x, f, the pair duals and the metric duals sorted by
 reference key (ConstraintKey.encode), plus max violation, nnz and the
 objectives (north_star: x within 1e-9 relative, objective within 1e-6 -- we
-require x bitwise and the objectives to 1e-12).
+require x bitwise, the primal objective to 1e-12 and the dual objective,
+a cancelling sum, to 1e-9).
 """
 
 import hashlib
@@ -46,7 +47,10 @@ def replay(config, fixture, passes=None, every=1):
         assert st.nnz_metric == g["nnz"][k], k
         assert st.steps == g["steps"][k], k
         assert st.primal_objective == pytest.approx(g["primal"][k], rel=1e-12, abs=1e-12), k
-        assert st.dual_objective == pytest.approx(g["dual"][k], rel=1e-12, abs=1e-9), k
+        # The dual objective sums ~C(n,2) terms with heavy cancellation (b.y - ||.||^2/2):
+        # the state is bitwise equal, only the summation order differs from numpy's
+        # pairwise dot, which moves the last few of its ~12 significant digits.
+        assert st.dual_objective == pytest.approx(g["dual"][k], rel=1e-9, abs=1e-9), k
         if (k + 1) % every and k + 1 != passes:
             continue
         x, f = sess.state()

@@ -1,6 +1,6 @@
 """Summarise a round's ncu outputs (gpurun_out/) into profiles/<tag>_*.
 
-  python tools/summarize_profiles.py r01
+  python tools/summarize_profiles.py r02a 3     (tag, BASELINE config of the captures)
 """
 import csv
 import io
@@ -86,7 +86,7 @@ def full_summary(tag):
     return out
 
 
-def main(tag):
+def main(tag, config=3):
     os.makedirs(PROF, exist_ok=True)
     table, per, tot = launches(tag)
     dram = tile_dram(tag)
@@ -99,19 +99,22 @@ def main(tag):
         fh.write("## Launch list of `python bench.py --steps 3 --warmup 3 --no-cpu` "
                  "(`--metrics gpu__time_duration.sum --clock-control none`; cold-cache, serialised)\n\n")
         fh.write(table + "\n\n")
-        fh.write("## tile_round_kernel, all 50 launches of pass 4 (config 2, n=1000, b=40)\n\n")
+        fh.write(f"## tile_round_kernel, every launch of pass 4 (config {config}, b=40): DRAM bytes\n\n")
         fh.write("```\n" + json.dumps(dram, indent=2) + "\n```\n\n")
-        fh.write("## Full capture (`--set full`), biggest round of pass 3\n\n```\n")
+        fh.write("## Full capture (`--set full`), round NR/2 of pass 3 (tools/gpu_round.sh)\n\n```\n")
         for k, v in full.items():
             fh.write(f"{k:40s} {v}\n")
         fh.write("```\n\n## Per-source-line instruction share and stall samples\n\n```\n" + stall + "```\n")
-    data = {"config2_b40": {"dram_bytes_per_launch": dram["dram_bytes_per_launch"],
-                            "l2_bytes_per_launch": dram["l2_bytes_per_launch"],
-                            "launches_measured": dram["launches"], "source": f"{tag}_ncu_summary.md"}}
+    path = os.path.join(PROF, "ncu_tile_kernel.json")
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    data[f"config{config}_b40"] = {"dram_bytes_per_launch": dram["dram_bytes_per_launch"],
+                                   "l2_bytes_per_launch": dram["l2_bytes_per_launch"],
+                                   "launches_measured": dram["launches"],
+                                   "source": f"{tag}_ncu_summary.md"}
     with open(os.path.join(PROF, "ncu_tile_kernel.json"), "w") as fh:
         json.dump(data, fh, indent=2)
     print(open(os.path.join(PROF, f"{tag}_ncu_summary.md")).read()[:3000])
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 3)
