@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(CUBE_WARPS * 32, 2) cube_level_kernel(CubeArgs
     cp_async_commit();
     if (tid < 8) zero[tid] = 0.0;
     WarpDuals *wd = wds + warp;
-    rd_init(wd, a.rp, cd.stream0 + warp, lane);
+    DualRegs dr;
+    rd_init(dr, wd, a.rp, cd.stream0 + warp, lane);
     cp_async_wait_all();
     __syncthreads();
 
@@ -102,7 +103,6 @@ __global__ void __launch_bounds__(CUBE_WARPS * 32, 2) cube_level_kernel(CubeArgs
     const int Lmin = Ic + Jc + Kc, Lmax = Lmin + 3 * c - 3;
     const StepConsts k = a.kc;
     const int64_t stream = cd.stream0 + warp;
-    uint32_t head = wd->head;
     double viol = 0.0;
     for (int L = Lmin; L <= Lmax; ++L) {
         uint32_t pa[S], pc[S], pe[S];
@@ -120,32 +120,29 @@ __global__ void __launch_bounds__(CUBE_WARPS * 32, 2) cube_level_kernel(CubeArgs
             any_bad |= bad[s];
         }
         const uint32_t base = (uint32_t)(L - Lmin) * (uint32_t)(S * 96);
-        if (__any_sync(0xffffffffu, any_bad) || head < base + (uint32_t)(S * 96)) {
+        if (__any_sync(0xffffffffu, any_bad) || dr.head < base + (uint32_t)(S * 96)) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const uint32_t bs = base + (uint32_t)(s * 96);
-                if (!(__any_sync(0xffffffffu, bad[s]) || head < bs + 96u)) continue;
-                double y[1][3] = {{0.0, 0.0, 0.0}};
-                if (head < bs + 96u) {
-                    rd_lookup<1>(wd, a.rp, bs, lane, y);
-                    head = wd->head;
-                }
+                if (!(__any_sync(0xffffffffu, bad[s]) || dr.head < bs + 96u)) continue;
                 double p = ld_sh(pa[s]), cx = ld_sh(pc[s]), e = ld_sh(pe[s]);
+                double y[3] = {0.0, 0.0, 0.0};
+                if (dr.head < bs + 96u) rd_lookup1(dr, wd, a.rp, bs, lane, y);
                 double th[3] = {0.0, 0.0, 0.0};
-                if (bad[s] | (y[0][0] != 0.0) | (y[0][1] != 0.0) | (y[0][2] != 0.0)) {
+                if (bad[s] | (y[0] != 0.0) | (y[1] != 0.0) | (y[2] != 0.0)) {
                     double wa = 1.0, wc = 1.0, we = 1.0;
                     if (!UNIT) {
                         wa = ld_sh(pa[s] + xb);
                         wc = ld_sh(pc[s] + xb);
                         we = ld_sh(pe[s] + xb);
                     }
-                    step3<UNIT>(p, cx, e, wa, wc, we, y[0], k, viol, th);
+                    step3<UNIT>(p, cx, e, wa, wc, we, y, k, viol, th);
                     st_sh(pa[s], p);
                     st_sh(pc[s], cx);
                     st_sh(pe[s], e);
                 }
                 if (__any_sync(0xffffffffu, (th[0] > THETA_FLOOR) | (th[1] > THETA_FLOOR) | (th[2] > THETA_FLOOR)))
-                    wr_append(wd, a.wp, a.ctr, stream, bs, lane, th[0], th[1], th[2]);
+                    wr_append(dr, wd, a.wp, a.ctr, stream, bs, lane, th[0], th[1], th[2]);
             }
         }
         __syncthreads();  // the next level reads this level's writes
@@ -159,7 +156,7 @@ __global__ void __launch_bounds__(CUBE_WARPS * 32, 2) cube_level_kernel(CubeArgs
             if (ar < bc && bc < n) a.x[(int64_t)ar * a.ld + bc] = blk[t * cc2 + e];
         }
     }
-    wr_finish(wd, a.wp, a.ctr, stream, lane);
+    wr_finish(dr, wd, a.wp, a.ctr, stream, lane);
     viol = warp_max(viol);
     if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
 }

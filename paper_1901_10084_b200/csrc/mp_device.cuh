@@ -133,7 +133,8 @@ struct TileArgs {
     int32_t round_id;           // schedule round of this launch
     int32_t lw;                 // active lanes per warp slot row (<= 32)
     int32_t colm;               // column-major slot map in each band
-    int32_t tl_round;           // MP_TIMELINE builds: round whose first tile is traced
+    int32_t tl_round;           // MP_TIMELINE builds: round whose tile tl_tile is traced
+    int32_t tl_tile;
     const void *tmap;           // 2-D TMA descriptor of x (box wkp x BLK), null: element copies
     int32_t wkp;                // WK row pitch in doubles (>= b; the TMA box width)
     int32_t wrp;                // WR row pitch in doubles (>= W)
@@ -505,127 +506,113 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned
 // ---------------------------------------------------------------------------
 // warp-stream reader (shared-memory staged, bulk-copy prefetch)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void rd_wait_buf(WarpDuals *w, int bf, int lane) {
-    const uint32_t ph = w->phase[bf];
-    mbar_wait(&w->mbar[bf], ph);
-    __syncwarp();
-    if (lane == 0) w->phase[bf] = ph ^ 1u;
-    __syncwarp();
-}
+// The cursor of a warp's read and write streams lives in registers (every
+// lane holds the same values; `wcidx`/`wnext` only matter in lane 0), so an
+// exact step's dual lookup and append cost no shared-memory round trips or
+// warp barriers for bookkeeping; only the chunk data is in shared memory.
+struct DualRegs {
+    uint32_t head;     // key of the next unconsumed entry, KEY_END when none
+    int32_t pos;       // its index in buf[cur]
+    int32_t cur;       // read buffer holding the current chunk
+    uint32_t ph;       // bit b: parity of buf[b]'s next bulk-copy completion
+    int32_t has_next;  // buf[cur ^ 1] holds (or is receiving) the next chunk
+    int32_t wstate;    // writer: -1 nothing written yet, -2 dead (pool overflow), 0 active
+    int32_t wfill;     // entries staged in wbuf[wcur]
+    int32_t wcur;      // staging buffer being filled
+    uint32_t wcount;   // entries written by this warp
+    int32_t wcidx;     // lane 0: pool index of the chunk staged in wbuf[wcur]
+    int32_t wnext;     // lane 0: pool index allocated ahead for the next chunk (-3: none yet)
+};
 
 // Start of a tile: load the stream's first chunk, prefetch the second.
-__device__ __forceinline__ void rd_init(WarpDuals *w, const DualPool &p, int64_t stream,
+__device__ __forceinline__ void rd_init(DualRegs &r, WarpDuals *w, const DualPool &p, int64_t stream,
                                         int lane) {
     if (lane == 0) {
         mbar_init(&w->mbar[0], 1);
         mbar_init(&w->mbar[1], 1);
-        w->phase[0] = w->phase[1] = 0;
-        w->cur = 0;
-        w->pos = 0;
-        w->wchunk = -1;
-        w->wfill = 0;
-        w->wcount = 0;
-        w->wcur = 0;
         mbar_fence_init();
     }
     __syncwarp();
+    r.ph = 0u;
+    r.cur = 0;
+    r.pos = 0;
+    r.wstate = -1;
+    r.wfill = 0;
+    r.wcur = 0;
+    r.wcount = 0u;
+    r.wcidx = -1;
+    r.wnext = -3;
     const int32_t c = p.head[stream];
     if (c >= 0) {
         if (lane == 0) bulk_load(&w->buf[0], &p.rec[c], sizeof(ChunkRec), &w->mbar[0]);
-        rd_wait_buf(w, 0, lane);
+        mbar_wait(&w->mbar[0], 0u);
+        r.ph = 1u;
         const int32_t nx = w->buf[0].next;
-        if (lane == 0) {
-            w->has_next = nx >= 0;
-            if (nx >= 0) bulk_load(&w->buf[1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[1]);
-            w->head = w->buf[0].keys[0];
-        }
-    } else if (lane == 0) {
-        w->has_next = 0;
-        w->head = KEY_END;
-        w->pos = CHUNK;
+        r.has_next = nx >= 0;
+        if (lane == 0 && nx >= 0) bulk_load(&w->buf[1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[1]);
+        r.head = w->buf[0].keys[0];
+    } else {
+        r.has_next = 0;
+        r.head = KEY_END;
+        r.pos = CHUNK;
     }
-    __syncwarp();
 }
 
-// Consume every entry with key in [base, base + S*96) (one level of this
-// warp's S slots); lane l receives y[s][kind] of its slots.  Warp-collective.
-template <int S>
-__device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint32_t base, int lane,
-                                          double (&y)[S][3]) {
-    const uint32_t lim = base + (uint32_t)(S * 96);
-    uint32_t head = w->head;
-    int pos = w->pos, cur = w->cur;
-#ifndef MP_EXP_NOFASTLOOKUP
-    // common case: one entry in range, not the chunk's last -- broadcast reads
-    if (head < lim && pos + 1 < CHUNK) {
-        const uint32_t nxt = w->buf[cur].keys[pos + 1];
-        if (nxt >= lim) {
-            const double v = w->buf[cur].vals[pos];
-            const uint32_t off = head - base;
-            const uint32_t sl = off / 96u, r = off - 96u * sl;
-            if (r / 3u == (uint32_t)lane) {
-                const uint32_t kd = r - 3u * (uint32_t)lane;
-#pragma unroll
-                for (int ss = 0; ss < S; ++ss)
-#pragma unroll
-                    for (int kk = 0; kk < 3; ++kk)
-                        if (sl == (uint32_t)ss && kd == (uint32_t)kk) y[ss][kk] = v;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                w->head = nxt;
-                w->pos = pos + 1;
-            }
-            __syncwarp();
-            return;
-        }
-    }
+// Consume every entry with key in [bs, bs + 96) (one slot of one level);
+// lane l receives y[kind] of its triplet.  Warp-collective, no loop over
+// entries: keys are sorted by (lane, kind), so an entry's chunk index is the
+// number of in-range entries before it, read off per-kind lane masks
+// (3 REDUX + POPC) -- each lane then loads its own values.
+__device__ __forceinline__ void rd_lookup1(DualRegs &r, WarpDuals *w, const DualPool &p, uint32_t bs,
+                                           int lane, double (&y)[3]) {
+    const uint32_t lim = bs + 96u;
+#ifdef MP_TIMELINE
+    if (lane == 0) w->wpad[2] += 1;
 #endif
-    while (head < lim) {
-        const uint32_t key = w->buf[cur].keys[lane];
-        const unsigned m = __ballot_sync(0xffffffffu, lane >= pos && key < lim);
-        unsigned mm = m;
-        while (mm) {
-            const int src = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const uint32_t off = w->buf[cur].keys[src] - base;
-            const uint32_t sl = off / 96u, r = off - 96u * sl;
-            if (r / 3u == (uint32_t)lane) {
-                const double v = w->buf[cur].vals[src];
-                const uint32_t kd = r - 3u * (uint32_t)lane;
-#pragma unroll
-                for (int ss = 0; ss < S; ++ss)
-#pragma unroll
-                    for (int kk = 0; kk < 3; ++kk)
-                        if (sl == (uint32_t)ss && kd == (uint32_t)kk) y[ss][kk] = v;
-            }
-        }
-        pos += __popc(m);
-        if (pos >= CHUNK) {
-            if (!w->has_next) {
-                head = KEY_END;
+    while (r.head < lim) {
+        const ChunkRec &c = w->buf[r.cur];
+        const uint32_t key = c.keys[lane];
+        const bool in = lane >= r.pos && key < lim;  // keys >= head >= bs
+        const uint32_t off = key - bs;
+        const uint32_t t = (off * 0xAAABu) >> 17;  // off / 3 (exact for off < 2^15)
+        const uint32_t kd = off - 3u * t;
+        const uint32_t bit = in ? (1u << (t & 31u)) : 0u;
+        const uint32_t T0 = __reduce_or_sync(0xffffffffu, kd == 0u ? bit : 0u);
+        const uint32_t T1 = __reduce_or_sync(0xffffffffu, kd == 1u ? bit : 0u);
+        const uint32_t T2 = __reduce_or_sync(0xffffffffu, kd == 2u ? bit : 0u);
+        const uint32_t below = (1u << lane) - 1u;
+        const int q = r.pos + __popc(T0 & below) + __popc(T1 & below) + __popc(T2 & below);
+        const int h0 = (int)((T0 >> lane) & 1u), h1 = (int)((T1 >> lane) & 1u), h2 = (int)((T2 >> lane) & 1u);
+        if (h0) y[0] = c.vals[q];
+        if (h1) y[1] = c.vals[q + h0];
+        if (h2) y[2] = c.vals[q + h0 + h1];
+        r.pos += __popc(T0) + __popc(T1) + __popc(T2);
+#ifdef MP_TIMELINE
+        if (lane == 0) w->wpad[0] += __popc(T0) + __popc(T1) + __popc(T2);
+#endif
+        if (r.pos >= CHUNK) {  // the level continues in (or the stream ends with) the next chunk
+            if (!r.has_next) {
+                r.head = KEY_END;
                 break;
             }
-            rd_wait_buf(w, cur ^ 1, lane);
-            cur ^= 1;
-            pos = 0;
-            const int32_t nx = w->buf[cur].next;
-            __syncwarp();  // everyone is done with the old buffer
-            if (lane == 0) {
-                w->has_next = nx >= 0;
-                if (nx >= 0) bulk_load(&w->buf[cur ^ 1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[cur ^ 1]);
-            }
-            __syncwarp();
+            const int nb = r.cur ^ 1;
+#ifdef MP_TIMELINE
+            const long long tw0 = clock64();
+#endif
+            mbar_wait(&w->mbar[nb], (r.ph >> nb) & 1u);
+#ifdef MP_TIMELINE
+            if (lane == 0) { w->wpad[1] += (int)(clock64() - tw0); w->wpad[2] += 1 << 16; }
+#endif
+            r.ph ^= 1u << nb;
+            __syncwarp();  // every lane is done with buf[cur] before it is refilled
+            r.cur = nb;
+            r.pos = 0;
+            const int32_t nx = w->buf[nb].next;
+            r.has_next = nx >= 0;
+            if (lane == 0 && nx >= 0) bulk_load(&w->buf[nb ^ 1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[nb ^ 1]);
         }
-        head = w->buf[cur].keys[pos];
+        r.head = w->buf[r.cur].keys[r.pos];
     }
-    __syncwarp();
-    if (lane == 0) {
-        w->head = head;
-        w->pos = pos;
-        w->cur = cur;
-    }
-    __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -635,7 +622,9 @@ __device__ __forceinline__ void rd_lookup(WarpDuals *w, const DualPool &p, uint3
 // pool with one bulk copy (cp.async.bulk, async proxy): no scattered global
 // stores on the exact-step path, and a later release fence does not wait for
 // them.  Two staging buffers: one filling, one possibly still being read by
-// its bulk copy.
+// its bulk copy.  From a stream's second chunk on, the pool index of the next
+// chunk is allocated one chunk ahead, so the allocation's atomic round trip
+// is off the exact-step path.
 // every lane that wrote the staged chunk: make its writes visible to the
 // async proxy; then (after __syncwarp) one lane issues the copy
 __device__ __forceinline__ void fence_proxy_async() {
@@ -651,9 +640,8 @@ __device__ __forceinline__ void bulk_wait_read_le1() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// One pool chunk index for this stream (lane 0; -1 on pool overflow).
-__device__ __forceinline__ int32_t wr_alloc(const DualPool &p, PassCounters *ctr) {
-    int32_t c = atomicAdd(&ctr->chunks_used, 1);
+// A pool index checked against the capacity (lane 0; -1 on pool overflow).
+__device__ __forceinline__ int32_t wr_check(int32_t c, const DualPool &p, PassCounters *ctr) {
     if (c >= p.cap) {
         atomicExch(&ctr->overflow, 1);
         c = -1;
@@ -661,7 +649,7 @@ __device__ __forceinline__ int32_t wr_alloc(const DualPool &p, PassCounters *ctr
     return c;
 }
 
-__device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassCounters *ctr,
+__device__ __forceinline__ void wr_append(DualRegs &r, WarpDuals *w, const DualPool &p, PassCounters *ctr,
                                           int64_t stream, uint32_t base, int lane, double t0,
                                           double t1, double t2) {
 #ifdef MP_EXP_NOAPPEND
@@ -671,102 +659,80 @@ __device__ __forceinline__ void wr_append(WarpDuals *w, const DualPool &p, PassC
     const unsigned m0 = __ballot_sync(0xffffffffu, h0);
     const unsigned m1 = __ballot_sync(0xffffffffu, h1);
     const unsigned m2 = __ballot_sync(0xffffffffu, h2);
-    int32_t chunk = w->wchunk;
-    if ((m0 | m1 | m2) == 0u || chunk == -2) return;
-    if (chunk == -1) {  // first entry of the stream: its first chunk
+    if ((m0 | m1 | m2) == 0u || r.wstate == -2) return;
+    if (r.wstate == -1) {  // first entry of the stream: its first chunk
+        int32_t c = 0;
         if (lane == 0) {
-            chunk = wr_alloc(p, ctr);
-            p.head[stream] = chunk >= 0 ? chunk : -1;
+            c = wr_check(atomicAdd(&ctr->chunks_used, 1), p, ctr);
+            p.head[stream] = c;
+            r.wcidx = c;
         }
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
-        if (chunk < 0) {
-            __syncwarp();
-            if (lane == 0) w->wchunk = -2;
-            __syncwarp();
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c < 0) {
+            r.wstate = -2;
             return;
         }
+        r.wstate = 0;
     }
     const unsigned lt = (1u << lane) - 1u;
     const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
     const int total = __popc(m0) + __popc(m1) + __popc(m2);
-    int fill = w->wfill, cur = w->wcur;
-    if (total == 1 && fill + 1 < CHUNK) {  // common case: one entry, room left
-        if (h0 | h1 | h2) {
-            w->wbuf[cur].keys[fill] = base + 3u * (uint32_t)lane + (h0 ? 0u : (h1 ? 1u : 2u));
-            w->wbuf[cur].vals[fill] = h0 ? t0 : (h1 ? t1 : t2);
-        }
-        __syncwarp();
-        if (lane == 0) {
-            w->wchunk = chunk;
-            w->wfill = fill + 1;
-            w->wcount += 1u;
-        }
-        __syncwarp();
-        return;
-    }
     // positions fill + before .. in key order (lane, kind); a position >= 32
     // belongs to a later chunk: write the window, flush, move on
     const double th[3] = {t0, t1, t2};
     const bool hk[3] = {h0, h1, h2};
-    int start = 0;  // stream position of wbuf[cur][0], relative to this append
+    int start = 0;  // stream position of wbuf[wcur][0], relative to this append
     while (true) {
-        int e = fill + before;
+        int e = r.wfill + before;
 #pragma unroll
         for (int kd = 0; kd < 3; ++kd) {
             if (hk[kd]) {
                 const int pos = e - start;
                 if (pos >= 0 && pos < CHUNK) {
-                    w->wbuf[cur].keys[pos] = base + 3u * (uint32_t)lane + (uint32_t)kd;
-                    w->wbuf[cur].vals[pos] = th[kd];
+                    w->wbuf[r.wcur].keys[pos] = base + 3u * (uint32_t)lane + (uint32_t)kd;
+                    w->wbuf[r.wcur].vals[pos] = th[kd];
                 }
                 ++e;
             }
         }
-        if (fill + total - start < CHUNK) break;
-        // wbuf[cur] is full: link it to a fresh chunk and send it
+        if (r.wfill + total - start < CHUNK) break;
+        // wbuf[wcur] is full: link it to the next chunk and send it
         int32_t nxt = 0;
         if (lane == 0) {
-            nxt = wr_alloc(p, ctr);
-            w->wbuf[cur].next = nxt;  // -1 on overflow: the pass is redone anyway
+            nxt = wr_check(r.wnext != -3 ? r.wnext : atomicAdd(&ctr->chunks_used, 1), p, ctr);
+            w->wbuf[r.wcur].next = nxt;  // -1 on overflow: the pass is redone anyway
         }
-        nxt = __shfl_sync(0xffffffffu, nxt, 0);
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-            bulk_store(&p.rec[chunk], &w->wbuf[cur], sizeof(ChunkRec));
+            bulk_store(&p.rec[r.wcidx], &w->wbuf[r.wcur], sizeof(ChunkRec));
             bulk_wait_read_le1();  // the other buffer's copy has read it
+            r.wcidx = nxt;
+            // allocate the chunk after `nxt` now; the value is first read at the next flush
+            r.wnext = nxt >= 0 ? atomicAdd(&ctr->chunks_used, 1) : -1;
         }
-        __syncwarp();
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
         if (nxt < 0) {
-            if (lane == 0) w->wchunk = -2;
-            __syncwarp();
+            r.wstate = -2;
             return;
         }
-        chunk = nxt;
-        cur ^= 1;
+        r.wcur ^= 1;
         start += CHUNK;
     }
-    __syncwarp();
-    if (lane == 0) {
-        w->wchunk = chunk;
-        w->wcur = cur;
-        w->wfill = fill + total - start;
-        w->wcount += (uint32_t)total;
-    }
-    __syncwarp();
+    r.wfill += total - start;
+    r.wcount += (uint32_t)total;
 }
 
-__device__ __forceinline__ void wr_finish(WarpDuals *w, const DualPool &p, PassCounters *ctr,
+__device__ __forceinline__ void wr_finish(DualRegs &r, WarpDuals *w, const DualPool &p, PassCounters *ctr,
                                           int64_t stream, int lane) {
-    const int32_t chunk = w->wchunk, fill = w->wfill, cur = w->wcur;
-    if (lane == 0 && w->wcount) atomicAdd(&ctr->nnz, (unsigned long long)w->wcount);
-    if (chunk >= 0) {
-        if (lane >= fill) w->wbuf[cur].keys[lane] = KEY_END;
-        if (lane == 0) w->wbuf[cur].next = -1;
+    if (lane == 0 && r.wcount) atomicAdd(&ctr->nnz, (unsigned long long)r.wcount);
+    if (r.wstate == 0) {
+        if (lane >= r.wfill) w->wbuf[r.wcur].keys[lane] = KEY_END;
+        if (lane == 0) w->wbuf[r.wcur].next = -1;
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) bulk_store(&p.rec[chunk], &w->wbuf[cur], sizeof(ChunkRec));
-    } else if (chunk == -1) {
+        if (lane == 0) bulk_store(&p.rec[r.wcidx], &w->wbuf[r.wcur], sizeof(ChunkRec));
+    } else if (r.wstate == -1) {
         if (lane == 0) p.head[stream] = -1;
     }
     if (lane == 0) bulk_wait_all();
@@ -1074,15 +1040,15 @@ __device__ __forceinline__ void slot_geom(SlotGeom<S> &G, const TileDesc &T, con
 #define MP_SLOT_INLINE __noinline__
 #endif
 template <int W, bool UNIT>
-__device__ MP_SLOT_INLINE double cold_slot(const CtaConst *cc, WarpDuals *wd, int warp, uint32_t base,
-                                         int pa, int pc, int pe, double viol, bool &fwd) {
+__device__ MP_SLOT_INLINE double cold_slot(const CtaConst *cc, WarpDuals *wd, DualRegs &dr, int warp,
+                                         uint32_t base, int pa, int pc, int pe, double viol, bool &fwd) {
     const int lane = threadIdx.x & 31;
-    double y[1][3] = {{0.0, 0.0, 0.0}};
-    if (wd->head < base + 96u) rd_lookup<1>(wd, cc->rp, base, lane, y);
     double p = ld_sh(pa), c = ld_sh(pc), e = ld_sh(pe);
+    double y[3] = {0.0, 0.0, 0.0};
+    if (dr.head < base + 96u) rd_lookup1(dr, wd, cc->rp, base, lane, y);
     double th[3] = {0.0, 0.0, 0.0};
-    const bool need = (fabs(__dsub_rn(p, c)) > e) | (__dsub_rn(e, p) > c) | (y[0][0] != 0.0) |
-                      (y[0][1] != 0.0) | (y[0][2] != 0.0);
+    const bool need = (fabs(__dsub_rn(p, c)) > e) | (__dsub_rn(e, p) > c) | (y[0] != 0.0) |
+                      (y[1] != 0.0) | (y[2] != 0.0);
     if (need) {
         double wa = 1.0, wc = 1.0, we = 1.0;
         if (!UNIT) {
@@ -1091,7 +1057,7 @@ __device__ MP_SLOT_INLINE double cold_slot(const CtaConst *cc, WarpDuals *wd, in
             wc = ld_sh(pc + xb);
             we = ld_sh(pe + xb);
         }
-        step3<UNIT>(p, c, e, wa, wc, we, y[0], cc->kc, viol, th);
+        step3<UNIT>(p, c, e, wa, wc, we, y, cc->kc, viol, th);
         st_sh(pa, p);
         st_sh(pc, c);
         st_sh(pe, e);
@@ -1100,7 +1066,7 @@ __device__ MP_SLOT_INLINE double cold_slot(const CtaConst *cc, WarpDuals *wd, in
     }
     const int64_t stream = cc->T.stream0 + (int64_t)cc->band * cc->nwc + warp;
     if (__any_sync(0xffffffffu, (th[0] > THETA_FLOOR) | (th[1] > THETA_FLOOR) | (th[2] > THETA_FLOOR)))
-        wr_append(wd, cc->wp, cc->ctr, stream, base, lane, th[0], th[1], th[2]);
+        wr_append(dr, wd, cc->wp, cc->ctr, stream, base, lane, th[0], th[1], th[2]);
     return viol;
 }
 
@@ -1109,8 +1075,8 @@ __device__ MP_SLOT_INLINE double cold_slot(const CtaConst *cc, WarpDuals *wd, in
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned char *sm,
                                            const SlotGeom<S> &G, const CtaConst *cc, WarpDuals *wd,
-                                           int warp, int b, int ihi, int klo, double (&xcr)[S],
-                                           uint32_t &head, double &viol, bool &fwd) {
+                                           DualRegs &dr, int warp, int b, int ihi, int klo,
+                                           double (&xcr)[S], double &viol, bool &fwd) {
     int pa[S], pc[S], pe[S];
     level_hot<S, W, ALIAS>(sm, G, L, b, ihi, klo, pa, pc, pe, xcr);
     bool moved = false;
@@ -1119,9 +1085,8 @@ __device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned
         const uint32_t bs = base0 + (uint32_t)(s * 96);
         const double a = ld_sh(pa[s]), c = ld_sh(pc[s]), e = ld_sh(pe[s]);
         const bool bad = (fabs(__dsub_rn(a, c)) > e) | (__dsub_rn(e, a) > c);
-        if (__any_sync(0xffffffffu, bad) || head < bs + 96u) {
-            viol = cold_slot<W, UNIT>(cc, wd, warp, bs, pa[s], pc[s], pe[s], viol, fwd);
-            head = wd->head;
+        if (__any_sync(0xffffffffu, bad) || dr.head < bs + 96u) {
+            viol = cold_slot<W, UNIT>(cc, wd, dr, warp, bs, pa[s], pc[s], pe[s], viol, fwd);
             if (!ALIAS) xcr[s] = ld_sh(pc[s]);  // the exact step may move x_ik
             moved = true;
         }
@@ -1134,8 +1099,8 @@ __device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned
 #endif
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned flagged,
-                                          const CtaConst *cc, WarpDuals *wd, int warp, double viol,
-                                          const SlotGeom<S> G) {
+                                          const CtaConst *cc, WarpDuals *wd, DualRegs &dr, int warp,
+                                          double viol, const SlotGeom<S> G) {
     const int lane = threadIdx.x & 31;
     const TileDesc &T = cc->T;
     const int b = cc->b, C = cc->C, band = cc->band;
@@ -1149,15 +1114,18 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
     // violated.  After a level that moved x the later levels are re-checked
     // with the new values (the hot test, all of them at once) instead of being
     // replayed one by one -- a replayed level with no violated row and no
-    // stored dual is a no-op in the reference.
+    // stored dual is a no-op in the reference.  The loop jumps from level to
+    // level: the next one is the next flagged level or the next holding a
+    // stored dual (the cursor's head key names its level).
     unsigned todo = flagged;
 #ifdef MP_TIMELINE
     long long tq0 = clock64(), c_lk = 0, c_mt = 0, c_ap = 0, c_ld = 0, nlev = 0;
+    __syncwarp();
+    if (lane == 0) wd->wpad[0] = wd->wpad[1] = wd->wpad[2] = 0;
+    __syncwarp();
 #endif
-    for (int Lc = first; Lc <= Le; ++Lc) {
+    for (int Lc = first; Lc <= Le;) {
         const uint32_t base = (uint32_t)(Lc - T.Lbeg) * PER_LEVEL;
-        const bool has_dual = wd->head < base + PER_LEVEL;
-        if (!has_dual && !((todo >> (Lc - L0)) & 1u)) continue;
 #ifdef MP_TIMELINE
         ++nlev;
         long long tq = clock64();
@@ -1168,13 +1136,14 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
 #pragma unroll
         for (int s = 0; s < S; ++s) {  // slot by slot: keys are ordered by slot
             const uint32_t bs = base + (uint32_t)(s * 96);
-            double y[1][3] = {{0.0, 0.0, 0.0}};
-            if (wd->head < bs + 96u) rd_lookup<1>(wd, cc->rp, bs, lane, y);
+            // the level's x loads go out before the lookup (independent)
+            double p = ld_sh(pa[s]), c = ld_sh(pc[s]), e = ld_sh(pe[s]);
+            double y[3] = {0.0, 0.0, 0.0};
+            if (dr.head < bs + 96u) rd_lookup1(dr, wd, cc->rp, bs, lane, y);
 #ifdef MP_TIMELINE
             { const long long t = clock64(); c_lk += t - tq; tq = t; }
 #endif
             double th[3] = {0.0, 0.0, 0.0};
-            double p = ld_sh(pa[s]), c = ld_sh(pc[s]), e = ld_sh(pe[s]);
             double wa = 1.0, wc = 1.0, we = 1.0;
             if (!UNIT) {
                 wa = ld_sh(pa[s] + xb);
@@ -1182,13 +1151,13 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
                 we = ld_sh(pe[s] + xb);
             }
             const bool need = (fabs(__dsub_rn(p, c)) > e) | (__dsub_rn(e, p) > c) |
-                              (y[0][0] != 0.0) | (y[0][1] != 0.0) | (y[0][2] != 0.0);
+                              (y[0] != 0.0) | (y[1] != 0.0) | (y[2] != 0.0);
             bool any_th = false;
 #ifdef MP_TIMELINE
             { const long long t = clock64(); c_ld += t - tq; tq = t; }
 #endif
             if (need) {
-                step3<UNIT>(p, c, e, wa, wc, we, y[0], k, viol, th);
+                step3<UNIT>(p, c, e, wa, wc, we, y, k, viol, th);
                 st_sh(pa[s], p);
                 st_sh(pc[s], c);
                 st_sh(pe[s], e);
@@ -1204,7 +1173,7 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
             { const long long t = clock64(); c_mt += t - tq; tq = t; }
 #endif
             if (__any_sync(0xffffffffu, any_th))
-                wr_append(wd, cc->wp, cc->ctr, stream, bs, lane, th[0], th[1], th[2]);
+                wr_append(dr, wd, cc->wp, cc->ctr, stream, bs, lane, th[0], th[1], th[2]);
 #ifdef MP_TIMELINE
             { const long long t = clock64(); c_ap += t - tq; tq = t; }
 #endif
@@ -1224,16 +1193,24 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
             }
             todo = (todo & ((2u << (Lc - L0)) - 1u)) | __reduce_or_sync(0xffffffffu, f);
         }
+        // next level to replay: flagged, or holding the next stored dual
+        const unsigned rest = todo & ~((2u << (Lc - L0)) - 1u);
+        int nxt = rest ? L0 + __ffs(rest) - 1 : Le + 1;
+        if (dr.head < (uint32_t)(Le + 1 - T.Lbeg) * PER_LEVEL)
+            nxt = min(nxt, T.Lbeg + (int)(dr.head / PER_LEVEL));
+        Lc = nxt;
     }
 #ifdef MP_TIMELINE
-    if (cc->tl && lane == 0) {  // the caller's batch record, slots 4..7
+    if (cc->tl && lane == 0) {  // the caller's batch record, slots 3..7
         const int nb = wd->pad;  // batch index parked by the caller
         if (nb < TL_MAXB) {
             unsigned long long *r = cc->trace + (((size_t)band * 16 + warp) * TL_MAXB + nb) * TL_REC;
             // lookup, x loads + check, exact step + stores + forwarding, append
             r[4] = (unsigned long long)c_lk | ((unsigned long long)nlev << 48);
-            r[5] = (unsigned long long)c_ld;
-            r[6] = (unsigned long long)c_mt;
+            // load+check | entries consumed << 32;  step | lookups, chunk switches << 32
+            r[5] = (unsigned long long)c_ld | ((unsigned long long)(unsigned)wd->wpad[0] << 32);
+            r[6] = (unsigned long long)c_mt | ((unsigned long long)(unsigned)wd->wpad[2] << 32);
+            r[3] = 1ull | ((unsigned long long)(unsigned)wd->wpad[1] << 8);
             r[7] = (unsigned long long)c_ap | ((unsigned long long)(clock64() - tq0) << 32);
         }
     }
@@ -1351,8 +1328,8 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
 // the update).
 template <int S, int W, bool UNIT, bool ALIAS>
 __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const SlotGeom<S> &G,
-                                      CtaConst &cc, TileSync &ts, WarpDuals *wd, int warp, int b,
-                                      int ihi, int klo, uint32_t &head, double &viol, int &nbatch) {
+                                      CtaConst &cc, TileSync &ts, WarpDuals *wd, DualRegs &dr, int warp,
+                                      int b, int ihi, int klo, double &viol, int &nbatch) {
     if (La > Lb) return;
     constexpr int U = MP_BATCH;
     constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
@@ -1452,7 +1429,7 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
         const unsigned wfl = __reduce_or_sync(0xffffffffu, fl);
         const uint32_t lim = base0 + (uint32_t)(Le - L + 1) * PER_LEVEL;
 #ifndef MP_EXP_NOCOLD
-        const bool go_cold = wfl != 0u || head < lim;
+        const bool go_cold = wfl != 0u || dr.head < lim;
 #else
         const bool go_cold = false;  // timing experiment only: results are wrong
 #endif
@@ -1460,14 +1437,13 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
         if (go_cold) {
             // first level that needs the exact step: flagged, or the next dual
             int first = wfl ? L + __ffs(wfl) - 1 : Le + 1;
-            if (head < lim) first = min(first, L + (int)((head - base0) / PER_LEVEL));
+            if (dr.head < lim) first = min(first, L + (int)((dr.head - base0) / PER_LEVEL));
 #ifdef MP_TIMELINE
             if (lane == 0) wd->pad = nbatch;
             __syncwarp();
 #endif
             if (S == 1) {
-                viol = cold_batch<S, W, UNIT, ALIAS>(L, first, Le, wfl, &cc, wd, warp, viol, G);
-                head = wd->head;
+                viol = cold_batch<S, W, UNIT, ALIAS>(L, first, Le, wfl, &cc, wd, dr, warp, viol, G);
                 if (!ALIAS) {  // the exact steps may have moved this thread's x_ik
 #pragma unroll
                     for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
@@ -1478,9 +1454,9 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
                 bool fwd = false, dirty = false;
                 for (int Lc = first; Lc <= Le; ++Lc) {
                     const uint32_t bl = (uint32_t)(Lc - T.Lbeg) * PER_LEVEL;
-                    if (!dirty && !((wfl >> (Lc - L)) & 1u) && !(head < bl + PER_LEVEL)) continue;
-                    dirty |= level_full<S, W, UNIT, ALIAS>(Lc, bl, sm, G, &cc, wd, warp, b, ihi, klo, xcr,
-                                                           head, viol, fwd);
+                    if (!dirty && !((wfl >> (Lc - L)) & 1u) && !(dr.head < bl + PER_LEVEL)) continue;
+                    dirty |= level_full<S, W, UNIT, ALIAS>(Lc, bl, sm, G, &cc, wd, dr, warp, b, ihi, klo, xcr,
+                                                           viol, fwd);
                 }
                 if (__any_sync(0xffffffffu, fwd)) fence_cluster();
             }
@@ -1497,7 +1473,7 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
             r[0] = (unsigned long long)tl0;
             r[1] = (unsigned long long)tl1;
             r[2] = (unsigned long long)clock64();
-            r[3] = go_cold ? 1ull : 0ull;
+            r[3] = go_cold ? (S == 1 ? r[3] : 1ull) : 0ull;  // cold_batch wrote 1 | chunk-wait cycles << 8
         }
 #endif
         ++nbatch;
@@ -1879,7 +1855,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.tma_st = a.tma_store && T.z - T.klo + 1 == b;
         cc.wkp = a.wkp;
         cc.wrp = a.wrp;
-        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == 0 && band < 8;
+        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == a.tl_tile && band < 8;
         cc.B32 = B32;
         cc.lw = a.lw;
         cc.colm = a.colm;
@@ -1929,7 +1905,8 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     cp_async_commit();
     if (tid < 16) ts.landed_by[tid] = hi0;  // every band lands the same prologue blocks
     WarpDuals *wd = wds + (warp < nwc ? warp : 0);
-    if (warp < nwc) rd_init(wd, a.rp, stream_base + warp, lane);
+    DualRegs dr;
+    if (warp < nwc) rd_init(dr, wd, a.rp, stream_base + warp, lane);
     cp_async_wait_all();
     if (tmap && tid == 0)
         for (int bk = lo0; bk <= hi0; ++bk) wk_tma_wait<W>(&ts, bk);
@@ -1954,7 +1931,6 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         SlotGeom<S> G;
         slot_geom<S, W>(G, T, M, B32, b, r0, r1, warp, lane, a.lw, a.colm != 0);
         const int ihi = T.ihi, klo = T.klo;
-        uint32_t head = wd->head;
         // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or
         // K) iff L in (2*ihi + z, 2*klo + ilo).
         const int mid_a = max(2 * ihi + T.z + 1, T.Lbeg);
@@ -1968,11 +1944,11 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 #endif
         int nbatch = 0;
         if (mid_a <= mid_b) {
-            sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
-            sweep<S, W, UNIT, false>(mid_a, mid_b, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
-            sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
+            sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
+            sweep<S, W, UNIT, false>(mid_a, mid_b, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
+            sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
         } else {
-            sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, warp, b, ihi, klo, head, viol, nbatch);
+            sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
         }
     }
 
@@ -2018,7 +1994,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     }
 #endif
     if (warp < nwc) {
-        wr_finish(wd, a.wp, a.ctr, stream_base + warp, lane);
+        wr_finish(dr, wd, a.wp, a.ctr, stream_base + warp, lane);
         viol = warp_max(viol);
         if (lane == 0) atomic_max_nonneg(&a.ctr->viol_bits, viol);
     }

@@ -848,6 +848,7 @@ TileArgs tile_args(mp_handle *h) {
     ta.kc = h->kc;
     ta.trace = h->trace;
     ta.tl_round = getenv("MP_TL_ROUND") ? atoi(getenv("MP_TL_ROUND")) : -1;
+    ta.tl_tile = getenv("MP_TL_TILE") ? atoi(getenv("MP_TL_TILE")) : 0;
     ta.eps = h->eps;
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[h->rp ^ 1];

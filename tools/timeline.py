@@ -55,15 +55,23 @@ if os.environ.get("TL_SUMMARY"):
     for c in bands:
         r = v[c, :15].reshape(-1, 8)
         r = r[r[:, 2] != 0]
-        cold = r[:, 3] == 1
+        cold = (r[:, 3] & 1) == 1
         rc = r[cold]
         lk = rc[:, 4] & ((1 << 48) - 1)
         nl = rc[:, 4] >> 48
         ap = rc[:, 7] & 0xFFFFFFFF
         tot = rc[:, 7] >> 32
+        ent = rc[:, 5] >> 32
+        ld = rc[:, 5] & 0xFFFFFFFF
+        st = rc[:, 6] & 0xFFFFFFFF
+        slow = (rc[:, 6] >> 32) & 0xFFFF
+        nsw = rc[:, 6] >> 48
+        wt = rc[:, 3] >> 8
         print(f"band {c}: cold batches {cold.sum():4d}  cold batch {np.mean(rc[:,2]-rc[:,1]):6.0f}  in call "
-              f"{tot.mean():6.0f} levels {nl.mean():.2f}  lookup {lk.mean():5.0f}  load+check {rc[:,5].mean():5.0f}  "
-              f"step {rc[:,6].mean():5.0f}  append {ap.mean():5.0f}  hot batch {np.mean(r[~cold,2]-r[~cold,1]):5.0f}")
+              f"{tot.mean():6.0f} levels {nl.mean():.2f}  lookup {lk.mean():5.0f}  load+check {ld.mean():5.0f}  "
+              f"step {st.mean():5.0f}  append {ap.mean():5.0f}  hot batch {np.mean(r[~cold,2]-r[~cold,1]):5.0f} | "
+              f"entries {ent.mean():.2f} slow lookups {slow.mean():.2f} chunk switches {nsw.mean():.2f} "
+              f"switch wait {wt.mean():.0f}")
     sys.exit(0)
 for c in bands:
     hdr = v[c, 15, 0]
@@ -79,7 +87,7 @@ for c in bands:
         r = r[:nb]
         wait = (r[:, 1] - r[:, 0]).sum()
         work = (r[:, 2] - r[:, 1]).sum()
-        cold = r[:, 3] == 1
+        cold = (r[:, 3] & 1) == 1
         gaps = r[1:, 0] - r[:-1, 2]
         if cold.any():
             rc = r[cold]
