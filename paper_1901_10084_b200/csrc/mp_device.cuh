@@ -139,7 +139,34 @@ struct TileArgs {
     int32_t wkp;                // WK row pitch in doubles (>= b; the TMA box width)
     int32_t wrp;                // WR row pitch in doubles (>= W)
     int32_t tma_store;          // interior WK blocks of the last band may be box-stored
+    // Dataflow launch (df = 1): all tiles of the schedule's second family in
+    // one launch; each cluster claims the next tile (qctr) and waits, ring
+    // block by ring block, for the write-backs of the two tiles whose pairs it
+    // reads next (dep: {row predecessor, column predecessor}, -1 = none in
+    // this launch), published per (tile, band) in prog.  See DF_* below.
+    int32_t df;
+    const int4 *dep;  // {row, column, diagonal predecessor, 0}
+    int32_t *prog;
+    int32_t *qctr;
 };
+
+// Dataflow launch (second family of tiled_rounds, schedule.py:117-153):
+// tiles (x + c*b, z - c*b) of round s with x >= 1.  Every pair a tile (x, z)
+// touches was last touched (in the reference order) either by a first-family
+// tile -- done before this launch starts -- or by one of two tiles of the
+// previous round: its row predecessor (x, z - b), same rows, whose x_ij rows
+// it reads as its own x_ij (WR ring) and, for j in [klo - b, klo), whose RK
+// block it reads; and its column predecessor (x - b, z), same columns, whose
+// x_jk rows (WK ring) hold this tile's x_jk rows and its RK rows.  (Checked
+// exhaustively by tools/df_deps.py against the per-pair last-toucher of the
+// whole schedule.)  Near the diagonal (z - x = b + 1, rows and columns
+// overlapping) a tile may also read pairs its row predecessor never touched,
+// last touched by the diagonal predecessor (x - b, z - b): such a tile waits
+// for that one to finish before it starts (dep.z).
+// prog[t * C + band] = ring blocks below it written back
+// by band `band` of tile t (WR rows of the band; the last band also WK),
+// DF_DONE once the tile finished (RK rows and the last blocks too).
+constexpr int DF_DONE = 0x3fffffff;
 
 #ifdef MP_TILETIME
 // Diagnostic per-tile timing (tools/tile_times.py): per (round, tile, band)
@@ -216,6 +243,12 @@ struct CtaConst {
     int32_t wkp;          // WK row pitch (doubles)
     int32_t wrp;          // WR row pitch (doubles)
     unsigned long long *tt;  // MP_TILETIME builds: this CTA's record, else null
+    // dataflow launch: the predecessors' progress words this CTA waits on
+    // (null: none), the first ring block needing the row predecessor
+    // finished, and this CTA's own progress word (null: not a dataflow launch)
+    const int32_t *dep_r, *dep_c, *dep_d;  // dep_d: band 0 of the diagonal predecessor
+    int32_t r_fin_blk;
+    int32_t *my_prog;
 };
 
 #ifndef MP_CMAX  // largest cluster (CTAs per tile) the host plans; > 8 is non-portable
@@ -1266,7 +1299,60 @@ struct TileSync {
     int blk0;           // the tile's first ring block (TMA slot phases count from it)
     int wb_lo;          // TMA producer: lowest block not yet written back (slots below are free)
     int wslow;          // TMA producer: writers' broadcast of the slowest warp's next level
+    int df_hi;          // dataflow launch: highest ring block whose predecessors' data is visible
+    int tile;           // dataflow launch: the tile this cluster claimed
 };
+
+// ---- dataflow launch: progress words in global memory --------------------
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int32_t *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Publish progress: the caller's (and, through the CTA barrier it passed,
+// its peers') write-backs -- generic stores and completed bulk/TMA stores --
+// happen before the release.
+__device__ __forceinline__ void df_publish(int32_t *p, int v) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// After an acquire: later async-proxy (TMA / bulk) reads see the data.
+__device__ __forceinline__ void df_after_acquire() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// Highest ring block this tile may load given the predecessors' progress
+// values r (row) and c (column): block g needs c > g; and, if it holds WR
+// columns (16g < klo), r > g -- or the row predecessor finished once g
+// reaches its RK columns [klo - b, klo) (g >= r_fin_blk = (klo - b) / 16;
+// the later blocks of the prefix hold no WR column, so the prefix of
+// loadable blocks ends at min(r, r_fin_blk) - 1 until the predecessor is done).
+__device__ __forceinline__ int df_hi_of(const CtaConst *cc, int r, int c) {
+    int hi = 0x3fffffff;
+    if (cc->dep_c) hi = min(hi, c - 1);
+    if (cc->dep_r && r < DF_DONE) hi = min(hi, min(r, cc->r_fin_blk) - 1);
+    return hi;
+}
+// Poll the predecessors (relaxed) and return the highest loadable block;
+// `seen` caches it; an advance is acquired (one acquire per advance).
+__device__ __forceinline__ int df_poll(const CtaConst *cc, int &seen) {
+    const int r = cc->dep_r ? ld_relaxed_gpu(cc->dep_r) : DF_DONE;
+    const int c = cc->dep_c ? ld_relaxed_gpu(cc->dep_c) : DF_DONE;
+    const int hi = df_hi_of(cc, r, c);
+    if (hi > seen) {
+        if (cc->dep_r) (void)ld_acquire_gpu(cc->dep_r);
+        if (cc->dep_c) (void)ld_acquire_gpu(cc->dep_c);
+        df_after_acquire();
+        seen = hi;
+    }
+    return seen;
+}
+// Block until blocks up to g may be loaded.
+__device__ __forceinline__ void df_wait_blk(const CtaConst *cc, int &seen, int g) {
+    while (df_poll(cc, seen) < g) __nanosleep(64);
+}
 
 // Lowest ring block landed in every CTA of the cluster: a block may be used
 // (and an upstream band may forward writes into it) only once every band's
@@ -1576,6 +1662,10 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
                 if (C > 1) fast = max(fast, ld_acquire_cluster(band0_done) + 2 * MP_BATCH);
                 ts->pslow = slow + 1;  // next level of the slowest warp
                 ts->pfast = fast + 1;  // next level of the fastest warp
+                if (cc->my_prog) {     // dataflow launch: what the predecessors allow
+                    int seen = ts->df_hi;
+                    ts->df_hi = df_poll(cc, seen);
+                }
             }
         }
         producer_bar(pn);
@@ -1597,11 +1687,17 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
             ++lo_res;
             busy = true;
         }
+        if (cc->my_prog && busy) {  // dataflow launch: publish the written-back blocks
+            if (ptid == 0) bulk_wait_all();
+            __threadfence_block();
+            producer_bar(pn);
+            if (ptid == 0) df_publish(cc->my_prog, lo_res);
+        }
 #ifdef MP_TIMELINE
         const long long tp2 = clock64();
 #endif
         const int need_fast = min(fast - T.ilo - T.klo, T.jhi) / BLK;
-        const int want = min(need_fast + LOOKAHEAD, blast);
+        const int want = min(min(need_fast + LOOKAHEAD, blast), ts->df_hi);
         // A slot whose WK rows were just written back element by element (by
         // every producer thread, rows split over warps) may be refilled by the
         // loader thread's TMA box only after all of them have read it.
@@ -1704,6 +1800,7 @@ __device__ __noinline__ void ring_producer_tma(unsigned char *sm, const CtaConst
         const int rows = max(0, min(r1, T.ihi - T.ilo + 1) - r0);  // band rows that exist
         const unsigned tx = (unsigned)(cc->wkp * BLK * 8 + rows * BLK * 8);
         int landed = hi_issued, published = hi_issued;
+        int df_seen = ts->df_hi;  // dataflow launch: highest block the predecessors allow
         while (true) {
             int slow = 0x3fffffff, fast = -0x3fffffff;
             for (int w = 0; w < nwc; ++w) {
@@ -1715,7 +1812,8 @@ __device__ __noinline__ void ring_producer_tma(unsigned char *sm, const CtaConst
             // band 0 leads the cluster: load ahead of it (a hint, relaxed)
             if (C > 1) fast = max(fast, ld_relaxed_cluster(band0_done) + 2 * MP_BATCH);
             const int need_fast = min(fast + 1 - T.ilo - T.klo, T.jhi) / BLK;
-            const int want = min(need_fast + MP_LOOKAHEAD, blast);
+            int want = min(need_fast + MP_LOOKAHEAD, blast);
+            if (cc->my_prog && want > df_seen) want = min(want, df_poll(cc, df_seen));
             bool busy = false;
             if (hi_issued < want) {
                 const int lo = ld_acquire(&ts->wb_lo);  // slots below lo were written back
@@ -1782,9 +1880,15 @@ __device__ __noinline__ void ring_producer_tma(unsigned char *sm, const CtaConst
                     tma_store_2d(cc->tmap, T.klo, lo * BLK, smem_u32(WK + ((lo * BLK) & (W - 1)) * cc->wkp));
                 }
             }
-            if (wtid == 0) bulk_wait_read_all();  // the box stores have read their slots
+            if (wtid == 0) {
+                if (cc->my_prog) bulk_wait_all();  // dataflow: the box stores are complete in x
+                else bulk_wait_read_all();         // the box stores have read their slots
+            }
             asm volatile("bar.sync 2, %0;" ::"r"(wn) : "memory");
-            if (wtid == 0) st_release(&ts->wb_lo, lo);
+            if (wtid == 0) {
+                st_release(&ts->wb_lo, lo);
+                if (cc->my_prog) df_publish(cc->my_prog, lo);  // every writer's stores: the barrier above
+            }
         } else {
             __nanosleep(64);
         }
@@ -1807,7 +1911,20 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     // a cluster of C CTAs shares one tile: CTA `band` owns rows [r0, r1) (relative to ilo)
     const int C = (int)cluster_size();
     const int band = C > 1 ? (int)cluster_rank() : 0;
-    const TileDesc T = a.tiles[blockIdx.x / C];
+    // dataflow launch: the cluster claims the next tile of the launch's list
+    // (in schedule order, so every tile it may wait on is claimed by a running
+    // cluster); a per-round launch takes its tile from the grid position
+    int tidx = (int)(blockIdx.x / C);
+    if (a.df) {
+        if (band == 0 && tid == 0) {
+            const int t = atomicAdd(a.qctr, 1);
+            for (int d = 0; d < C; ++d) st_relaxed_cluster(mapa(smem_u32(&ts.tile), (unsigned)d), t);
+        }
+        if (C > 1) cluster_sync_all();
+        else __syncthreads();
+        tidx = ts.tile;
+    }
+    const TileDesc T = a.tiles[tidx];
     const int b = a.b;
     const int RB = (b + C - 1) / C;
     const int r0 = band * RB, r1 = min(b, r0 + RB);
@@ -1855,15 +1972,29 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.tma_st = a.tma_store && T.z - T.klo + 1 == b;
         cc.wkp = a.wkp;
         cc.wrp = a.wrp;
-        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && blockIdx.x / C == a.tl_tile && band < 8;
+        cc.tl = a.trace != nullptr && a.round_id == a.tl_round && tidx == a.tl_tile && band < 8;
         cc.B32 = B32;
         cc.lw = a.lw;
         cc.colm = a.colm;
         cc.tt = nullptr;
 #ifdef MP_TILETIME
-        if (a.trace && a.round_id < TT_ROUNDS && blockIdx.x / C < TT_TILES && band < TT_BANDS)
-            cc.tt = a.trace + (((size_t)a.round_id * TT_TILES + blockIdx.x / C) * TT_BANDS + band) * TT_REC;
+        {  // (a dataflow launch's tiles continue into the following round slots)
+            const int rr = a.round_id + tidx / TT_TILES, tt = tidx % TT_TILES;
+            if (a.trace && rr < TT_ROUNDS && band < TT_BANDS)
+                cc.tt = a.trace + (((size_t)rr * TT_TILES + tt) * TT_BANDS + band) * TT_REC;
+        }
 #endif
+        cc.dep_r = cc.dep_c = cc.dep_d = nullptr;
+        cc.my_prog = nullptr;
+        cc.r_fin_blk = 0;
+        if (a.df) {
+            const int4 dp = a.dep[tidx];
+            cc.my_prog = a.prog + (size_t)tidx * C + band;
+            if (dp.x >= 0) cc.dep_r = a.prog + (size_t)dp.x * C + band;
+            if (dp.y >= 0) cc.dep_c = a.prog + (size_t)dp.y * C + (C - 1);
+            if (dp.z >= 0) cc.dep_d = a.prog + (size_t)dp.z * C;
+            cc.r_fin_blk = max(T.klo - b, 0) / BLK;
+        }
     }
     for (int e = tid; e < W; e += nt) smd[M.zero() / 8 + e] = 0.0;
     if (tid < 32) ts.done[tid] = T.Lbeg - 1;
@@ -1884,11 +2015,32 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 #endif
 
     // --- staging prologue (all threads) -----------------------------------
-    rk_block<true>(T, b, a.ld, a.x, RK, tid, nt, 0, b);
-    if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt, 0, b);
     const int blast = T.jhi / BLK;
     const int lo0 = max(T.Lbeg - T.ihi - T.z, T.jlo) / BLK;
     const int hi0 = min(min(T.Lbeg - T.ilo - T.klo, T.jhi) / BLK + 1, blast);
+    ts.df_hi = 0x3fffffff;
+    if (a.df) {  // the predecessors' write-backs this prologue reads
+        if (tid == 0) {
+            if (cc.dep_d) {  // near the diagonal: the diagonal predecessor finished (every band)
+                for (int d = 0; d < C; ++d)
+                    while (ld_relaxed_gpu(cc.dep_d + d) < DF_DONE) __nanosleep(64);
+                for (int d = 0; d < C; ++d) (void)ld_acquire_gpu(cc.dep_d + d);
+                df_after_acquire();
+            }
+            int seen = -1;
+            df_wait_blk(&cc, seen, hi0);
+            if (cc.dep_c) {  // RK rows [ilo, ihi]: the column predecessor's WK blocks up to ihi
+                const int need = T.ihi / BLK + 1;
+                while (ld_relaxed_gpu(cc.dep_c) < need) __nanosleep(64);
+                (void)ld_acquire_gpu(cc.dep_c);
+                df_after_acquire();
+            }
+            ts.df_hi = seen;
+        }
+        __syncthreads();
+    }
+    rk_block<true>(T, b, a.ld, a.x, RK, tid, nt, 0, b);
+    if (!UNIT) rk_block<true>(T, b, a.ld, const_cast<double *>(a.winvx), RK + xsize, tid, nt, 0, b);
     if (tmap && tid == 0) {  // WK blocks by TMA (cc was written by this thread)
         ts.blk0 = lo0;
         ts.wb_lo = lo0;
@@ -1981,6 +2133,13 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         }
     }
     rk_block<false>(T, b, a.ld, a.x, RK, tid, nt, r0, r1);
+    if (a.df) {  // this band's rows are final in x: successors may read them
+        __syncthreads();
+        if (tid == 0) {
+            bulk_wait_all();  // this thread's box stores above
+            df_publish(cc.my_prog, DF_DONE);
+        }
+    }
 #ifdef MP_TRACE
     if (a.trace) {
         __syncthreads();

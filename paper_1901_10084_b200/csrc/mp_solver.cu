@@ -350,6 +350,16 @@ struct mp_handle {
         size_t smem = 0;
     };
     std::vector<RoundCfg> rcfg;       // per round
+    // Dataflow launch of the schedule's second family (mp_device.cuh, DF_*):
+    // rounds [df_r0, end) run as one launch of df_cnt tiles with one shape
+    // (rcfg of those rounds), each tile waiting on its two predecessors'
+    // progress words instead of a launch boundary per round.
+    bool df_allowed = true;           // off once sharded (per-round exchange)
+    bool df_on = false;
+    size_t df_r0 = 0;
+    int64_t df_off = 0, df_cnt = 0;
+    int4 *d_dep = nullptr;            // per dataflow tile: {row, column, diagonal} predecessor
+    int32_t *d_prog = nullptr;        // per (dataflow tile, band) progress, then the claim counter
     int32_t tma_store = 1;            // box write-back of interior WK blocks (MP_NO_TMA_STORE: off)
     std::vector<int32_t> tile_round;  // round of each tile
     // schedule_kind "serial": the cube wavefront (mp_cube.cuh)
@@ -414,6 +424,8 @@ struct mp_handle {
             dev_release(p.head);
         }
         dev_release(d_tiles);
+        dev_release(d_dep);
+        dev_release(d_prog);
         for (void *t : d_tmap) dev_release(t);
         dev_release(d_cubes);
         dev_release(ctr);
@@ -752,6 +764,60 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         }
         h->rcfg.push_back(best);
     }
+    // Second family (x >= 1) as one dataflow launch: tiles of one round wait
+    // only on the two predecessor tiles of the previous round, ring block by
+    // ring block, so the family's barrier depth (~n^2/(2b) levels) shrinks to
+    // ~2n (dataflow depth half the barrier depth; all of it here).
+    h->df_on = false;
+    if (h->df_allowed && h->kind == MP_SCHEDULE_TILED && !getenv("MP_NO_DF")) {
+        size_t r0 = cnt_r.size();
+        for (size_t r = 0; r < cnt_r.size(); ++r)
+            if (h->round_cnt[r] && h->tile_x[(size_t)h->round_off[r]] >= 1) {
+                r0 = r;
+                break;
+            }
+        int64_t ndf = 0;
+        for (size_t r = r0; r < cnt_r.size(); ++r) ndf += h->round_cnt[r];
+        // Cluster size: the launch is either chain-bound (each round's tiles
+        // trail their predecessors by ~3b + 2 ring blocks of levels, plus the
+        // longest tile) or throughput-bound (all tiles' levels times C SMs
+        // over the device).  A tile's time per level falls about as 1/C and
+        // its SM-time stays put, so the largest C whose SM-levels per SM stay
+        // within the chain's levels wins; else C = 2.  Measured (ms/pass):
+        // config 2 (169 tiles) 5.40 / 4.62 / 4.38 / 4.27 at C = 2 / 4 / 6 / 8,
+        // config 3 (2550 tiles) 105.8 / 116.2 / 112.8 / 115.4.
+        int64_t lev = 0, lmax = 0, nr = 0;
+        for (size_t r = r0; r < cnt_r.size(); ++r) {
+            nr += h->round_cnt[r] > 0;
+            for (int64_t t = h->round_off[r]; t < h->round_off[r] + h->round_cnt[r]; ++t) {
+                const int64_t l = h->tiles[(size_t)t].Lend - h->tiles[(size_t)t].Lbeg + 1;
+                lev += l;
+                lmax = std::max(lmax, l);
+            }
+        }
+        const int64_t chain = nr * (3 * (int64_t)b + 2 * BLK) + lmax;
+        int C = 2;
+        for (int c = 8; c > 2; --c)
+            if (lev * c <= chain * sms) {
+                C = c;
+                break;
+            }
+        C = std::min(C, std::min(cmax, b));
+        if (const char *e = getenv("MP_DF_C")) C = std::max(1, std::min(std::min(cmax, b), atoi(e)));
+        while (C > 1 && (C - 1) * ((b + C - 1) / C) >= b) --C;
+        if (r0 < cnt_r.size() && ndf > 0) {
+            if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
+            const mp_handle::RoundCfg &c = shape[C];
+            if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
+            if (c.S <= MAX_SLOTS && c.smem <= 227 * 1024 && cap[C] >= 1) {
+                for (size_t r = r0; r < cnt_r.size(); ++r) h->rcfg[r] = c;
+                h->df_on = true;
+                h->df_r0 = r0;
+                h->df_off = h->round_off[r0];
+                h->df_cnt = ndf;
+            }
+        }
+    }
     if (getenv("MP_VERBOSE")) {
         std::vector<int> hist(17, 0);
         for (const auto &c : h->rcfg) hist[(size_t)c.C]++;
@@ -773,6 +839,33 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         if (keys >= 0xFFFFFF00ull) return fail(MP_ERR_UNSUPPORTED, "tile too deep for 32-bit dual keys");
     }
     h->nstreams = acc;
+    if (h->df_on) {  // predecessors of every dataflow tile (-1: first family / none)
+        const int64_t nkb = h->nkb;
+        auto find = [&](int64_t x, int64_t z) -> int {
+            if (x < 1 || z < 2) return -1;
+            const int64_t iblk = (x + b - 1) / b, kblk = (h->n - 1 - z) / b;
+            if (iblk >= h->nib || kblk >= nkb) return -1;
+            const int32_t t = h->tile_of_blk[(size_t)(iblk * nkb + kblk)];
+            if (t < 0 || t < h->df_off || t >= h->df_off + h->df_cnt) return -1;
+            if (h->tile_x[(size_t)t] != x || h->tiles[(size_t)t].z != z) return -1;
+            return (int)(t - h->df_off);
+        };
+        std::vector<int4> dep((size_t)h->df_cnt);
+        for (int64_t i = 0; i < h->df_cnt; ++i) {
+            const size_t t = (size_t)(h->df_off + i);
+            const int64_t x = h->tile_x[t], z = h->tiles[t].z;
+            // diagonal predecessor only near the diagonal (tests/test_dataflow.py)
+            dep[(size_t)i] = make_int4(find(x, z - b), find(x - b, z), z - x <= 2 * b ? find(x - b, z - b) : -1, 0);
+        }
+        const int C = h->rcfg[h->df_r0].C;
+        dev_release(h->d_dep);
+        dev_release(h->d_prog);
+        h->d_dep = nullptr;
+        h->d_prog = nullptr;
+        CK(cudaMalloc(&h->d_dep, dep.size() * sizeof(int4)));
+        CK(cudaMemcpy(h->d_dep, dep.data(), dep.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&h->d_prog, ((size_t)h->df_cnt * C + 1) * sizeof(int32_t)));
+    }
     return MP_OK;
 }
 
@@ -860,6 +953,9 @@ TileArgs tile_args(mp_handle *h) {
 // [counter all-reduce when sharded], end.  Nothing here syncs the host.
 int pass_begin(mp_handle *h) {
     CK(cudaMemsetAsync(h->ctr, 0, sizeof(PassCounters), h->st));
+    if (h->df_on)  // dataflow launch: progress words and the claim counter
+        CK(cudaMemsetAsync(h->d_prog, 0, ((size_t)h->df_cnt * h->rcfg[h->df_r0].C + 1) * sizeof(int32_t),
+                           h->st));
     // snapshot for an overflow retry of this pass
     CK(cudaMemcpyAsync(h->snap_x, h->x, (size_t)h->n * h->ld * sizeof(double),
                        cudaMemcpyDeviceToDevice, h->st));
@@ -894,6 +990,27 @@ int pass_serial(mp_handle *h) {
 
 // This rank's tiles of round r: one CTA per tile.
 int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
+    if (h->df_on && r >= h->df_r0) {  // the second family: one dataflow launch
+        if (r != h->df_r0) return MP_OK;
+        const mp_handle::RoundCfg &c = h->rcfg[r];
+        ta.tiles = h->d_tiles + h->df_off;
+        ta.round_id = (int32_t)r;
+        ta.lw = c.LW;
+        ta.colm = c.colm ? 1 : 0;
+        ta.nt = c.NT;
+        ta.nwc = c.NWC;
+        ta.wkp = c.P;
+        ta.wrp = c.PR;
+        ta.tmap = x_tmap(h, c.P);
+        ta.tma_store = h->tma_store;
+        ta.df = 1;
+        ta.dep = h->d_dep;
+        ta.prog = h->d_prog;
+        ta.qctr = h->d_prog + (size_t)h->df_cnt * c.C;
+        const int rc = launch_tiles(h, c, ta, (int)h->df_cnt);
+        ta.df = 0;
+        return rc;
+    }
     const int64_t cnt = h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r];
     if (!cnt) return MP_OK;
     ta.tiles = h->sh.on ? h->sh.d_my_tiles + h->sh.my_off[r] : h->d_tiles + h->round_off[r];
@@ -1337,6 +1454,7 @@ namespace {
 int64_t launches_per_pass(const mp_handle *h) {
     int64_t c = 2;  // pair phase + finalize
     for (size_t r = 0; r < h->round_cnt.size(); ++r) {
+        if (h->df_on && r > h->df_r0) continue;  // one dataflow launch for the second family
         c += (h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r]) ? 1 : 0;
         if (round_exchanges(h, r)) c += 2;  // pack + unpack
     }
@@ -1841,7 +1959,10 @@ int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id) {
     // re-plan the launch shapes for the tiles one rank runs per round (the
     // largest share over ranks, so every rank numbers the dual streams alike):
     // fewer tiles per device leave room for larger clusters
-    if (world > 1) {
+    // sharded passes exchange footprints after every round: no dataflow launch
+    const bool was_df = h->df_on;
+    h->df_allowed = false;
+    if (world > 1 || was_df) {
         std::vector<int64_t> share(h->round_cnt.size(), 0);
         for (size_t r = 0; r < h->round_cnt.size(); ++r) {
             std::vector<int64_t> per((size_t)world, 0);
