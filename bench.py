@@ -298,6 +298,45 @@ def run_gpu(args):
     inst = instances.config_instance(args.config)
     n, b = inst.n, args.tile_b
     rows = rows_per_pass(n)
+    copies = 1 if args.sharded else ws  # instances the job solves
+
+    # ---- end to end through the public API (host buffers), run first: the
+    # session's device buffers are allocated inside the timed region --------
+    total = args.warmup + args.steps
+    if ws > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    if args.sharded:
+        from paper_1901_10084_b200.distributed import ShardedSession
+        shs = ShardedSession(inst, b, device=local)
+        stats = shs.run(total)
+        xs, fs = shs.state()
+        dk, dv = shs.duals()
+        shs.close()
+
+        class _Sol:  # the fields the JSON line reads
+            pass
+        sol = _Sol()
+        sol.stats = [type("S", (), {"primal_objective": s_.primal_objective,
+                                    "max_violation": s_.max_violation}) for s_ in stats]
+        sol.duals = type("D", (), {"nnz": staticmethod(lambda: len(dk))})
+    else:
+        sol = solve(inst, SolverConfig(tile_size=b, fixed_passes=total, device=local))
+    t_e2e = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    m = inst.npairs
+    h2d = 8 * 4 * m  # d, w, reg_x, reg_f
+    d2h = total * 64 + 8 * 2 * m + 16 * m + 16 * sol.duals.nnz()
+    # pass 1 is cheaper than the others (no stored duals yet, no exact steps
+    # from duals): timed, but its rows are not counted
+    e2e = {"value": copies * (total - 1) * rows / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": h2d / total, "d2h_bytes_per_step": d2h / total,
+           "wall_s": t_e2e, "passes": total, "passes_counted": total - 1,
+           "note": "first call in the process (cold device-buffer cache: every cudaMalloc inside); "
+                   "rows of passes 2..W+K counted, all passes timed"}
 
     # ---- device-resident timing ------------------------------------------------
     if args.sharded:  # one instance over all ranks (strong scaling)
@@ -330,7 +369,6 @@ def run_gpu(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_dev, metric_ms = float(tt[0]), float(tt[1])
     sess.close()
-    copies = 1 if args.sharded else ws
     value = copies * args.steps * rows / t_dev
 
     # ---- roofline of the dominant kernel (tile_round_kernel) ------------------
@@ -356,39 +394,6 @@ def run_gpu(args):
     roofline["whole_pass"] = {"bytes_per_pass": pass_bytes / args.steps,
                               "achieved": pass_bytes / t_dev / 1e9,
                               "frac": pass_bytes / t_dev / 1e9 / peak}
-
-    # ---- end to end through the public API (host buffers) ---------------------
-    total = args.warmup + args.steps
-    if ws > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    if args.sharded:
-        from paper_1901_10084_b200.distributed import ShardedSession
-        shs = ShardedSession(inst, b, device=local)
-        stats = shs.run(total)
-        xs, fs = shs.state()
-        dk, dv = shs.duals()
-        shs.close()
-
-        class _Sol:  # the fields the JSON line reads
-            pass
-        sol = _Sol()
-        sol.stats = [type("S", (), {"primal_objective": s_.primal_objective,
-                                    "max_violation": s_.max_violation}) for s_ in stats]
-        sol.duals = type("D", (), {"nnz": staticmethod(lambda: len(dk))})
-    else:
-        sol = solve(inst, SolverConfig(tile_size=b, fixed_passes=total, device=local))
-    t_e2e = time.perf_counter() - t0
-    if ws > 1:
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_e2e = float(tt[0])
-    m = inst.npairs
-    h2d = 8 * 4 * m  # d, w, reg_x, reg_f
-    d2h = total * 64 + 8 * 2 * m + 16 * m + 16 * sol.duals.nnz()
-    e2e = {"value": copies * total * rows / t_e2e, "unit": UNIT,
-           "h2d_bytes_per_step": h2d / total, "d2h_bytes_per_step": d2h / total,
-           "wall_s": t_e2e, "passes": total}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
