@@ -333,6 +333,9 @@ struct mp_handle {
     double eps = 0.0;
     bool unit_x = true, unit_f = true;
     StepConsts kc{};
+    // max over rows of #{j : d_ij < 1/2} over its mean: hub rows (Chung-Lu
+    // graphs) make the longest tiles of the small rounds exact-step bound
+    double hub = 1.0;
 
     // device state (x and winvx dense n x ld; the rest packed C(n,2))
     double *x = nullptr, *winvx = nullptr;
@@ -614,7 +617,7 @@ double ring_waves(const mp_handle::RoundCfg &c, int b, int pitch, bool wk) {
 // with at most 15 compute warps (any S is correct: a warp waits until its
 // predecessor finished the whole batch), up to 3 producer warps, W = 256
 // ring when it fits.
-mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
+mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1) {
     mp_handle::RoundCfg c;
     const int b = h->b;
     c.C = C;
@@ -640,8 +643,9 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C) {
         const int lw = c.RB * (32 / c.RB), s = slots_per_thread(lw);
         if (s <= slots_per_thread(32) && (slots + lw * s - 1) / (lw * s) <= MAX_CTA_THREADS / 32 - 3) c.LW = lw;
     }
-    if (const char *e = getenv("MP_LANES"))  // cluster rounds only (one CTA needs them all)
-        if (C > 1) c.LW = std::max(1, std::min(32, atoi(e)));
+    if (lanes < 0)
+        if (const char *e = getenv("MP_LANES")) lanes = atoi(e);
+    if (lanes > 0 && C > 1) c.LW = std::max(1, std::min(32, lanes));  // cluster rounds only (one CTA needs them all)
     const int LW = c.LW;
     S = slots_per_thread(LW);
     c.S = S;
@@ -719,6 +723,26 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     minc = std::min(minc, cmax);
     int64_t minc_cnt = sms * 3 / 8;  // 55 on B200 (50: config 3 128 ms, 55: 123 ms, 64: config 4 +1.4%)
     if (const char *e = getenv("MP_MIN_C_CNT")) minc_cnt = atoll(e);
+    // Hub instances (h->hub >= 8): the small rounds' longest tiles hold the
+    // hub rows and are exact-step bound; 8 bands of few-lane warps (the
+    // fewest lanes, whole band columns, with <= 14 compute warps) spread a
+    // row's exact steps over more warps.  Measured, config 3 (hub 83):
+    // 105.7 -> 95.3 ms/pass (C = 8 with 30 / 20 / 15 lanes: 104.4 / 98.9 /
+    // 95.3); config 2 (hub 1.6) would lose 2% with it, so it stays off there.
+    bool hubby = h->hub >= 8.0 && !getenv("MP_NO_HUB");
+    mp_handle::RoundCfg hub_shape;
+    if (hubby) {
+        const int C = std::min(8, std::min(cmax, b));
+        const int RB = (b + C - 1) / C;
+        int lw = 32;
+        for (int l = RB; l <= 32; l += RB)
+            if ((RB * b + l - 1) / l <= MAX_CTA_THREADS / 32 - 2) {
+                lw = l;
+                break;
+            }
+        hub_shape = round_shape(h, C, lw);
+        hubby = C > 1 && (C - 1) * RB < b && hub_shape.S <= MAX_SLOTS && hub_shape.smem <= 227 * 1024;
+    }
     std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
     std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
     std::vector<bool> have(17, false);
@@ -750,7 +774,9 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
             }
         }
         // small rounds: at least minc CTAs per tile (see minc above)
-        if (best.C < minc && cnt > 0 && cnt <= minc_cnt && (minc - 1) * ((b + minc - 1) / minc) < b) {
+        if (hubby && cnt > 0 && cnt <= minc_cnt) {
+            best = hub_shape;
+        } else if (best.C < minc && cnt > 0 && cnt <= minc_cnt && (minc - 1) * ((b + minc - 1) / minc) < b) {
             if (!have[minc]) shape[minc] = round_shape(h, minc), have[minc] = true;
             if (shape[minc].S <= MAX_SLOTS && shape[minc].smem <= 227 * 1024) best = shape[minc];
         }
@@ -806,10 +832,10 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         if (const char *e = getenv("MP_DF_C")) C = std::max(1, std::min(std::min(cmax, b), atoi(e)));
         while (C > 1 && (C - 1) * ((b + C - 1) / C) >= b) --C;
         if (r0 < cnt_r.size() && ndf > 0) {
-            if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
-            const mp_handle::RoundCfg &c = shape[C];
-            if (cap[C] < 0) cap[C] = max_active_clusters(h, c);
-            if (c.S <= MAX_SLOTS && c.smem <= 227 * 1024 && cap[C] >= 1) {
+            int lanes = 0;
+            if (const char *e = getenv("MP_DF_LANES")) lanes = atoi(e);
+            const mp_handle::RoundCfg c = round_shape(h, C, lanes);
+            if (c.S <= MAX_SLOTS && c.smem <= 227 * 1024 && max_active_clusters(h, c) >= 1) {
                 for (size_t r = r0; r < cnt_r.size(); ++r) h->rcfg[r] = c;
                 h->df_on = true;
                 h->df_r0 = r0;
@@ -1304,6 +1330,24 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
             if (!(inst->reg_f[p] > 0.0)) return bail(fail(MP_ERR_ARG, "regularization weights must be positive"));
             if (inst->reg_f[p] != 1.0) h->unit_f = false;
         }
+
+    // ---- hub factor of the instance (plan_rounds) ------------------------------
+    if (h->kind != MP_SCHEDULE_SERIAL) {
+        std::vector<int32_t> deg((size_t)n, 0);
+        int64_t p = 0;
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = i + 1; j < n; ++j, ++p)
+                if (inst->d_flat[p] < 0.5) {
+                    ++deg[(size_t)i];
+                    ++deg[(size_t)j];
+                }
+        int64_t sum = 0;
+        int32_t mx = 0;
+        for (int32_t v : deg) sum += v, mx = std::max(mx, v);
+        const double mean = (double)sum / (double)n;
+        h->hub = mx / std::max(mean, 1.0);
+        if (getenv("MP_VERBOSE")) fprintf(stderr, "[mp] hub factor %.1f (max degree %d, mean %.1f)\n", h->hub, mx, mean);
+    }
 
     // ---- schedule (schedule.tiled_rounds, schedule.py:117-153) -------------
     h->nib = (n + b - 1) / b + 2;
