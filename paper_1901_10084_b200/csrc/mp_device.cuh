@@ -927,6 +927,16 @@ struct SmemMap {
     __device__ __host__ int xbytes() const { return up(rk() + b * b * 8); }
 };
 
+// Lanes per warp slot row of a band with fewer real rows than the launch's
+// bands (the single-row tiles): the band's slots spread evenly over all its
+// compute warps (a hub row's exact steps then fall on many warps).  The host
+// encodes / decodes dual keys with the same map (mp_solver.cu).
+__host__ __device__ inline int band_lanes(int lw, int nwc, int S, int rows, int rb, int b, bool colm) {
+    if (!colm || rows >= rb) return lw;
+    const int per = nwc * S;
+    return max(1, min(lw, (rows * b + per - 1) / per));
+}
+
 template <int S>
 struct SlotGeom {
     int ik8[S];       // (i + k) * 8
@@ -1451,7 +1461,8 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
     const int *loc_flag = &ts.done[warp > 0 ? warp - 1 : 0];
     int rem_warp = cc.nwc - 1;
     if (cc.colm) {
-        const int r0 = cc.band * cc.RB, rbc = max(1, min(b, r0 + cc.RB) - r0);
+        const int r0 = cc.band * cc.RB;
+        const int rbc = max(1, min(min(b, r0 + cc.RB), T.ihi - T.ilo + 1) - r0);  // the band's real rows
         const int qmax = min(warp * lwS + lwS - 1, rbc * b - 1);
         const int kmax = max(qmax, 0) / rbc;
         rem_warp = min(cc.nwc - 1, (kmax * cc.RB + cc.RB - 1) / lwS);
@@ -1928,7 +1939,15 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     const int b = a.b;
     const int RB = (b + C - 1) / C;
     const int r0 = band * RB, r1 = min(b, r0 + RB);
-    const bool last_band = band == C - 1;
+    // Bands holding rows: all C, except for the first family's single-row
+    // tiles (x = 1 - b: row 0 only), which run on band 0 alone -- the other
+    // CTAs of the cluster only take part in its two barriers (no forwarding
+    // to them, no lattice coupling; band 0 writes WK back).  The slot map of
+    // a band covers its real rows (a single row's columns fill few warps).
+    const int nrows = T.ihi - T.ilo + 1;
+    const int Ce = min(C, (nrows + RB - 1) / RB);
+    const bool idle_band = band >= Ce;
+    const bool last_band = band == Ce - 1;
     const int64_t stream_base = T.stream0 + (int64_t)band * nwc;
     const SmemMap<W> M{b, RB, a.wkp, a.wrp};
     // TMA boxes need a 16-byte aligned start column: tiles with an odd klo copy
@@ -1959,7 +1978,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.xsize = xsize;
         cc.trace = a.trace;
         cc.kc = a.kc;
-        cc.C = C;
+        cc.C = Ce;  // the cluster as far as the sweep is concerned (bands with rows)
         cc.band = band;
         cc.RB = RB;
         cc.nwc = nwc;
@@ -1974,7 +1993,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.wrp = a.wrp;
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && tidx == a.tl_tile && band < 8;
         cc.B32 = B32;
-        cc.lw = a.lw;
+        cc.lw = band_lanes(a.lw, nwc, S, max(1, min(r1, nrows) - r0), r1 - r0, b, a.colm != 0);
         cc.colm = a.colm;
         cc.tt = nullptr;
 #ifdef MP_TILETIME
@@ -2071,7 +2090,12 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 #endif
 
     double viol = 0.0;
-    if (warp >= nwc) {
+    if (idle_band) {  // no rows: nothing to sweep; the epilogue writes back nothing of it
+        if (tid == 0) {
+            ts.lo_res = lo0;
+            ts.hi_issued = hi0;
+        }
+    } else if (warp >= nwc) {
         // (one CTA per tile: 40 WR rows per block are too many bulk copies for
         // one loader thread; the combined producer is faster there, config 5)
         if (UNIT && tmap && np >= 3 && C > 1 && !MP_OLD_PRODUCER)
@@ -2081,7 +2105,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     } else {
         // --- per-slot geometry: q = warp*32*S + s*32 + lane -> (i,k) -------
         SlotGeom<S> G;
-        slot_geom<S, W>(G, T, M, B32, b, r0, r1, warp, lane, a.lw, a.colm != 0);
+        slot_geom<S, W>(G, T, M, B32, b, r0, min(r1, nrows), warp, lane, cc.lw, a.colm != 0);
         const int ihi = T.ihi, klo = T.klo;
         // Level L touches j in [L-ihi-z, L-ilo-klo]: alias-free (no j in R or
         // K) iff L in (2*ihi + z, 2*klo + ilo).

@@ -732,7 +732,8 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     bool hubby = h->hub >= 8.0 && !getenv("MP_NO_HUB");
     mp_handle::RoundCfg hub_shape;
     if (hubby) {
-        const int C = std::min(8, std::min(cmax, b));
+        int C = std::min(8, std::min(cmax, b));
+        if (const char *e = getenv("MP_HUB_C")) C = std::max(2, std::min(std::min(cmax, b), atoi(e)));
         const int RB = (b + C - 1) / C;
         int lw = 32;
         for (int l = RB; l <= 32; l += RB)
@@ -740,6 +741,7 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
                 lw = l;
                 break;
             }
+        if (const char *e = getenv("MP_HUB_LANES")) lw = std::max(1, std::min(32, atoi(e)));
         hub_shape = round_shape(h, C, lw);
         hubby = C > 1 && (C - 1) * RB < b && hub_shape.S <= MAX_SLOTS && hub_shape.smem <= 227 * 1024;
     }
@@ -1219,8 +1221,12 @@ Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
     const uint32_t lvl = key / per_level, rem = key % per_level;
     const int s = (int)(rem / 96u), r2 = (int)(rem % 96u);
     const int lane = r2 / 3, kind = r2 % 3;
-    const int64_t q = ((int64_t)wb * c.S + s) * c.LW + lane;
-    const int64_t r0 = (int64_t)band * c.RB, rbc = std::max<int64_t>(1, std::min<int64_t>(h->b, r0 + c.RB) - r0);
+    // a band's slot map covers its real rows (single-row tiles: band 0, 1 row)
+    const int64_t nrows = (int64_t)T.ihi - T.ilo + 1;
+    const int64_t r0 = (int64_t)band * c.RB, r1 = std::min<int64_t>(h->b, r0 + c.RB),
+                  rbc = std::max<int64_t>(1, std::min<int64_t>(r1, nrows) - r0);
+    const int64_t LW = band_lanes(c.LW, c.NWC, c.S, (int)rbc, (int)(r1 - r0), h->b, c.colm);
+    const int64_t q = ((int64_t)wb * c.S + s) * LW + lane;
     const int64_t ii = c.colm ? r0 + q % rbc : r0 + q / h->b;
     const int64_t kk = c.colm ? q / rbc : q % h->b;
     Decoded d;
@@ -1822,9 +1828,11 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         const TileDesc &T = h->tiles[(size_t)t];
         const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[(size_t)t]];
         const int64_t band = (i - T.ilo) / c.RB, S = c.S;
-        const int64_t r0 = band * c.RB, rbc = std::max<int64_t>(1, std::min<int64_t>(b, r0 + c.RB) - r0);
+        const int64_t nrows = (int64_t)T.ihi - T.ilo + 1;
+        const int64_t r0 = band * c.RB, r1 = std::min<int64_t>(b, r0 + c.RB),
+                      rbc = std::max<int64_t>(1, std::min<int64_t>(r1, nrows) - r0);
         const int64_t q = c.colm ? (k - T.klo) * rbc + (i - T.ilo - r0) : (i - T.ilo - r0) * b + (k - T.klo);
-        const int64_t LW = c.LW;
+        const int64_t LW = band_lanes(c.LW, c.NWC, c.S, (int)rbc, (int)(r1 - r0), (int)b, c.colm);
         const int64_t w = q / (LW * S), s = (q % (LW * S)) / LW, lane = q % LW;
         const int64_t lvl = i + j + k - T.Lbeg;
         const uint32_t key32 = (uint32_t)(((lvl * S + s) * 96) + lane * 3 + kind);
