@@ -63,6 +63,28 @@
 
 namespace mp {
 
+// Checked builds (-DMP_CHECKED, tools/checked_tests.sh): device-side bounds
+// and protocol assertions -- every shared-memory access inside the dynamic
+// window, forwarded stores inside the replicated regions, dual-pool chunk
+// indices below the pool capacity, dual keys strictly increasing per stream
+// and never behind the read cursor, global ring addresses inside x, and
+// dataflow predecessors claimed before their successors.  (compute-sanitizer
+// is not available on this GPU pool; these checks stand in for it.)
+#ifdef MP_CHECKED
+#define MP_ASSERT(c)                                                                        \
+    do {                                                                                    \
+        if (!(c)) {                                                                         \
+            printf("MP_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                      \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define MP_ASSERT(c) \
+    do {             \
+    } while (0)
+#endif
+
 constexpr double THETA_FLOOR = 1e-15;  // _kernels.py:20
 constexpr int BLK = 16;                // j-block width of the streamed rings
 // levels per progress publish (batch) of a compute warp
@@ -267,6 +289,8 @@ __device__ __forceinline__ bool forward_jk(const CtaConst *cc, uint32_t ue, doub
     return false;  // timing experiment only: results are wrong
 #endif
     const int C = cc->C, band = cc->band;
+    MP_ASSERT((ue >= cc->rep_lo && ue < cc->zero_lo) || (ue >= cc->rk_lo && ue < cc->rk_lo + 8u * (uint32_t)(cc->b * cc->b)) ||
+              (ue < cc->rep_lo));  // WK, RK, or a WR value (not forwarded: dlast = band)
     int dlast = band;
     if (ue >= cc->rep_lo && ue < cc->zero_lo) {
         dlast = C - 1;
@@ -441,14 +465,27 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+#ifdef MP_CHECKED
+extern __shared__ __align__(1024) unsigned char mp_dyn_smem[];
+__device__ __forceinline__ void chk_sh(uint32_t a) {
+    uint32_t sz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sz));
+    const uint32_t lo = (uint32_t)__cvta_generic_to_shared(mp_dyn_smem);
+    MP_ASSERT(a >= lo && a + 8u <= lo + sz && (a & 7u) == 0u);
+}
+#else
+__device__ __forceinline__ void chk_sh(uint32_t) {}
+#endif
 // 32-bit shared-window addresses: the per-slot constants already hold the
 // absolute address, so the hot loop issues LDS [R] with no base add
 __device__ __forceinline__ double ld_sh(uint32_t a) {
+    chk_sh(a);
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
 __device__ __forceinline__ void st_sh(uint32_t a, double v) {
+    chk_sh(a);
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
@@ -555,6 +592,10 @@ struct DualRegs {
     uint32_t wcount;   // entries written by this warp
     int32_t wcidx;     // lane 0: pool index of the chunk staged in wbuf[wcur]
     int32_t wnext;     // lane 0: pool index allocated ahead for the next chunk (-3: none yet)
+#ifdef MP_CHECKED
+    uint32_t wlast;    // last key appended (keys must increase strictly)
+    int32_t wany;
+#endif
 };
 
 // Start of a tile: load the stream's first chunk, prefetch the second.
@@ -575,6 +616,10 @@ __device__ __forceinline__ void rd_init(DualRegs &r, WarpDuals *w, const DualPoo
     r.wcount = 0u;
     r.wcidx = -1;
     r.wnext = -3;
+#ifdef MP_CHECKED
+    r.wlast = 0u;
+    r.wany = 0;
+#endif
     const int32_t c = p.head[stream];
     if (c >= 0) {
         if (lane == 0) bulk_load(&w->buf[0], &p.rec[c], sizeof(ChunkRec), &w->mbar[0]);
@@ -602,6 +647,7 @@ __device__ __forceinline__ void rd_lookup1(DualRegs &r, WarpDuals *w, const Dual
 #ifdef MP_TIMELINE
     if (lane == 0) w->wpad[2] += 1;
 #endif
+    MP_ASSERT(r.head >= bs);  // every earlier level's entries were consumed
     while (r.head < lim) {
         const ChunkRec &c = w->buf[r.cur];
         const uint32_t key = c.keys[lane];
@@ -616,6 +662,7 @@ __device__ __forceinline__ void rd_lookup1(DualRegs &r, WarpDuals *w, const Dual
         const uint32_t below = (1u << lane) - 1u;
         const int q = r.pos + __popc(T0 & below) + __popc(T1 & below) + __popc(T2 & below);
         const int h0 = (int)((T0 >> lane) & 1u), h1 = (int)((T1 >> lane) & 1u), h2 = (int)((T2 >> lane) & 1u);
+        MP_ASSERT(!(h0 | h1 | h2) || q + h0 + h1 + h2 <= CHUNK);
         if (h0) y[0] = c.vals[q];
         if (h1) y[1] = c.vals[q + h0];
         if (h2) y[2] = c.vals[q + h0 + h1];
@@ -642,6 +689,7 @@ __device__ __forceinline__ void rd_lookup1(DualRegs &r, WarpDuals *w, const Dual
             r.pos = 0;
             const int32_t nx = w->buf[nb].next;
             r.has_next = nx >= 0;
+            MP_ASSERT(nx < p.cap);
             if (lane == 0 && nx >= 0) bulk_load(&w->buf[nb ^ 1], &p.rec[nx], sizeof(ChunkRec), &w->mbar[nb ^ 1]);
         }
         r.head = w->buf[r.cur].keys[r.pos];
@@ -710,6 +758,16 @@ __device__ __forceinline__ void wr_append(DualRegs &r, WarpDuals *w, const DualP
     const unsigned lt = (1u << lane) - 1u;
     const int before = __popc(m0 & lt) + __popc(m1 & lt) + __popc(m2 & lt);
     const int total = __popc(m0) + __popc(m1) + __popc(m2);
+#ifdef MP_CHECKED
+    {  // the smallest key of this append is above the stream's last one
+        const uint32_t kmin = base + 3u * (uint32_t)(__ffs(m0 | m1 | m2) - 1);
+        MP_ASSERT(!r.wany || kmin > r.wlast);
+        const int hl = 31 - __clz((int)(m0 | m1 | m2));
+        r.wlast = base + 3u * (uint32_t)hl + 2u;
+        r.wany = 1;
+    }
+    MP_ASSERT(lane != 0 || (r.wcidx >= 0 && r.wcidx < p.cap));
+#endif
     // positions fill + before .. in key order (lane, kind); a position >= 32
     // belongs to a later chunk: write the window, flush, move on
     const double th[3] = {t0, t1, t2};
@@ -808,6 +866,7 @@ __device__ __forceinline__ void ring_block(const TileDesc &T, int b, int p, int 
             if (!(v0 | v1)) continue;
             const uint32_t s = smem_u32(wr + ii * pr + (j & (W - 1)));
             double *gp = g + (int64_t)i * ld + j;
+            MP_ASSERT(i >= 0 && j >= 0 && j + 1 < ld + 1 && i < j + 1);
             if (v0 & v1) {
                 if (LOAD) cp_async16(s, gp);
                 else st_global_v2(gp, s);
@@ -1934,6 +1993,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         if (C > 1) cluster_sync_all();
         else __syncthreads();
         tidx = ts.tile;
+        MP_ASSERT(tidx >= 0 && tidx < (int)(gridDim.x / C));
     }
     const TileDesc T = a.tiles[tidx];
     const int b = a.b;
@@ -2008,6 +2068,7 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.r_fin_blk = 0;
         if (a.df) {
             const int4 dp = a.dep[tidx];
+            MP_ASSERT(dp.x < tidx && dp.y < tidx && dp.z < tidx);  // claimed before this tile
             cc.my_prog = a.prog + (size_t)tidx * C + band;
             if (dp.x >= 0) cc.dep_r = a.prog + (size_t)dp.x * C + band;
             if (dp.y >= 0) cc.dep_c = a.prog + (size_t)dp.y * C + (C - 1);
