@@ -662,6 +662,15 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1) {
     if (h->unit_x && fits(256, b, 256)) c.W = 256;
     if (h->unit_x && C > 1 && S <= 2 && fits(512, b, 512)) c.W = 512;
     if (const char *e = getenv("MP_RING_W")) c.W = std::min(c.W, std::max(128, atoi(e)));
+    // Progress needs the ring to hold the slowest warp's whole j-window: the
+    // producer frees blocks below slow - ihi - z and the warp reads up to
+    // slow - ilo - klo, a span of 2b - 2, plus the block being loaded.  (b <=
+    // 48 fits W = 128; larger tiles need W = 256, which only W = I has.)
+    const int need_blocks = (2 * b - 2 + BLK) / BLK + 2;
+    if (c.W / BLK < need_blocks) {  // no such shape: callers skip S > MAX_SLOTS
+        c.S = MAX_SLOTS + 1;
+        return c;
+    }
     // Row pitches against bank conflicts: the lanes of a warp read x_ij at
     // WR[i][j % W] and x_jk at WK[j % W][k] with j = L - i - k, so with the
     // plain pitches (W, b) lanes with equal i + k (or equal i mod 2 when b =
@@ -696,6 +705,22 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1) {
     return c;
 }
 
+// The shape every round can fall back to: one CTA per tile, or -- for tiles
+// too big for one CTA (b > 48: more than MAX_SLOTS slots per thread) -- the
+// smallest cluster that holds a tile (its rounds then run in waves).  C = 0:
+// no shape fits.
+mp_handle::RoundCfg fallback_shape(const mp_handle *h, int cmax) {
+    const int b = h->b;
+    for (int C = 1; C <= std::min(cmax, std::max(b, 1)); ++C) {
+        if (C > 1 && (C - 1) * ((b + C - 1) / C) >= b) continue;
+        const mp_handle::RoundCfg c = round_shape(h, C);
+        if (c.S <= MAX_SLOTS && c.smem <= 227 * 1024) return c;
+    }
+    mp_handle::RoundCfg none;
+    none.C = 0;
+    return none;
+}
+
 // Launch shape per round: a round with few tiles spreads each tile over a
 // cluster of C SMs (row bands, mp_device.cuh), as large as the device can
 // co-schedule for all of the round's tiles at once (cnt[r] = tiles one
@@ -707,9 +732,10 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const mp_handle::RoundCfg one = round_shape(h, 1);
     int cmax = MP_CMAX;
     if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(MP_CMAX, atoi(e)));
+    const mp_handle::RoundCfg one = fallback_shape(h, cmax);
+    if (one.C == 0) return fail(MP_ERR_UNSUPPORTED, "tile size %d does not fit the device's launch shapes", b);
     int fb = 2;  // cluster size for rounds whose clusters do not all fit at once
     if (const char *e = getenv("MP_WAVE_C")) fb = atoi(e);
     fb = std::min(fb, cmax);
@@ -1278,8 +1304,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         return fail(MP_ERR_UNSUPPORTED, "schedule_kind 'serial' is limited to n <= 20000 on the device");
     const int b = cfg->schedule_kind == MP_SCHEDULE_DIAGONAL ? 1 : cfg->tile_b;
     if (b < 1) return fail(MP_ERR_ARG, "tile size must be >= 1, got %d", b);
-    if (b > 48 && cfg->schedule_kind != MP_SCHEDULE_SERIAL)
-        return fail(MP_ERR_UNSUPPORTED, "tile size %d > 48 is not supported on the device", b);
+    if (b > 128 && cfg->schedule_kind != MP_SCHEDULE_SERIAL)
+        return fail(MP_ERR_UNSUPPORTED, "tile size %d > 128 is not supported on the device", b);
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -1380,10 +1406,11 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     }
     // Launch shape per round and dual-stream numbering (plan_rounds)
     if (h->kind != MP_SCHEDULE_SERIAL) {
-        const mp_handle::RoundCfg one = round_shape(h, 1);
-        if (one.S > MAX_SLOTS || one.smem > 227 * 1024)
-            return bail(fail(MP_ERR_UNSUPPORTED, "tile size %d does not fit one CTA", b));
+        const auto tp0 = std::chrono::steady_clock::now();
         const int rc0 = plan_rounds(h, h->round_cnt);
+        if (getenv("MP_VERBOSE"))
+            fprintf(stderr, "[mp] plan_rounds %.3f s\n",
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
         if (rc0) return bail(rc0);
     }
     if (h->kind == MP_SCHEDULE_SERIAL) {
@@ -1435,7 +1462,11 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     TRY(cudaMalloc(&h->x, dense));
     TRY(cudaMemsetAsync(h->x, 0, dense, h->st));  // x = 0 (solver.py:112)
     TRY(cudaMalloc(&h->snap_x, dense));
+    const auto tm0 = std::chrono::steady_clock::now();
     if ((rc = make_x_tmap(h))) return bail(rc);
+    if (getenv("MP_VERBOSE"))
+        fprintf(stderr, "[mp] make_x_tmap %.3f s\n",
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - tm0).count());
     h->tma_store = getenv("MP_NO_TMA_STORE") ? 0 : 1;
     tmark("x+tmap");
     TRY(cudaMalloc(&h->tmp, m * sizeof(double)));
