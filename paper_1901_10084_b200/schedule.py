@@ -99,12 +99,6 @@ class Round:
         return sum(u.size for u in self.units)
 
 
-def serial_order(n):
-    if n < 3:
-        raise ValueError(f"need n >= 3, got {n}")
-    return itertools.combinations(range(n), 3)
-
-
 def _anti_diagonal(x, z, b):
     out = []
     c = 0
@@ -164,37 +158,6 @@ def tile_level_order(tile, n):
     return sorted(trips, key=lambda t: (sum(t), (t[0] - ilo) * tile.b + (t[2] - klo)))
 
 
-class WorkerPlan:
-    """Static assignment of round units to workers (schedule.py:184-215)."""
-
-    def __init__(self, rounds, p):
-        if p < 1:
-            raise ValueError(f"need at least one worker, got {p}")
-        self.p = p
-        self.rounds = rounds
-        self.by_round = []
-        for rnd in rounds:
-            lanes = [[] for _ in range(p)]
-            for pos, unit in enumerate(rnd.units):
-                lanes[rnd.worker_of(pos, p)].append(unit)
-            self.by_round.append(lanes)
-
-    def worker_units(self, w):
-        for lanes in self.by_round:
-            yield from lanes[w]
-
-    def worker_triplets(self, w, n):
-        for unit in self.worker_units(w):
-            yield from unit_triplets(unit, n)
-
-    def worker_load(self, w):
-        return sum(u.size for u in self.worker_units(w))
-
-
-def worker_plan(rounds, p):
-    return WorkerPlan(rounds, p)
-
-
 def verify_partition(rounds, n):
     """Every triplet in exactly one unit (schedule.py:222-232)."""
     seen = [t for rnd in rounds for u in rnd.units for t in unit_triplets(u, n)]
@@ -215,28 +178,13 @@ def verify_independence(rounds, n):
 
 
 # ---------------------------------------------------------------------------
-# device mapping (mirrors mp_create in csrc/mp_solver.cu)
+# schedule depth
 # ---------------------------------------------------------------------------
 
-def cta_shape(b, max_threads=512):
-    """(slots per thread S, compute warps, producer warps) of mp_create: b*b
-    (i,k) pairs map to q = warp*32*S + s*32 + lane, b <= 32*S so lattice
-    neighbours sit in the same or the previous warp."""
-    s = max(1, (b + 31) // 32)
-    while (b * b + 32 * s - 1) // (32 * s) > max_threads // 32 - 1:
-        s += 1
-    nwc = (b * b + 32 * s - 1) // (32 * s)
-    return s, nwc, min(3, max_threads // 32 - nwc)
-
-
-def launch_plan(n, b):
-    """Per round, the CTAs of its launch: list of lists of (x, z, Lbeg, Lend)."""
-    return [[(t.x, t.z, *t.levels()) for t in rnd.units] for rnd in tiled_rounds(n, b)]
-
-
 def critical_levels(n, b):
-    """Sum over rounds of the deepest tile's level count: the number of
-    dependent __syncthreads() steps in one pass."""
+    """Barrier depth of a pass: sum over rounds of the deepest tile's level
+    count (the device runs the second family as one dataflow
+    launch, whose depth is far smaller, see tests/test_dataflow.py)."""
     total = 0
     for rnd in tiled_rounds(n, b):
         if rnd.units:

@@ -89,12 +89,6 @@ def test_tile_level_ranges(n, b):
             assert min(sums) == lo and max(sums) == hi
 
 
-def test_cta_shape():
-    for b in (1, 2, 8, 16, 32, 40, 48):
-        s, nwc, npw = schedule.cta_shape(b)
-        assert s * nwc * 32 >= b * b and b <= 32 * s and npw >= 1 and 32 * (nwc + npw) <= 512
-
-
 @pytest.mark.parametrize("n,c", [(11, 3), (17, 4), (20, 5), (23, 8)])
 def test_cube_order_equals_serial(n, c):
     """The cube-blocked wavefront (cube levels, then L levels inside a cube)
