@@ -162,13 +162,17 @@ def measured_peak():
 
 
 def ncu_traffic(config, b):
-    """dram bytes per tile-kernel launch from the committed ncu capture, if any."""
+    """DRAM bytes (read + write) of one pass's tile_round_kernel launches from
+    the committed ncu capture (profiles/ncu_tile_kernel.json), if any -- the
+    same unit as ``achieved`` (a pass's algorithmic bytes over its time)."""
     path = os.path.join(ROOT, "profiles", "ncu_tile_kernel.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        key = f"config{config}_b{b}"
-        return d.get(key, {}).get("dram_bytes_per_launch")
+        e = d.get(f"config{config}_b{b}", {})
+        if "dram_bytes_per_pass" in e:
+            return e["dram_bytes_per_pass"]
+        return None
     except (OSError, ValueError):
         return None
 
@@ -379,16 +383,16 @@ def run_gpu(args):
     if args.sharded:  # metric_bytes covers the whole instance: compare with the whole box
         peak *= ws
         peak_src += f" x {ws} GPUs"
-    n_rounds = sum(1 for r in schedule.tiled_rounds(n, b) if r.units)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config, b),
+                "traffic_unit": "DRAM bytes per pass (ncu, all tile_round_kernel launches of pass 4)",
                 "kernel": "tile_round_kernel", "peak_source": peak_src,
                 "frac_of_8TBs_nominal": achieved / 8000.0,
                 "algorithmic_bytes_per_pass": 16 * tx + 12 * nnz_io / max(args.steps, 1),
                 "T_x": tx, "metric_phase_share": metric_ms / (t_dev * 1e3),
-                "launches_per_pass": n_rounds + 2,
-                "critical_levels_per_pass": schedule.critical_levels(n, b),
-                "ns_per_level": metric_ms * 1e6 / args.steps / schedule.critical_levels(n, b)}
+                "launches_per_pass": launches / max(args.steps, 1),
+                "barrier_levels_per_pass": schedule.critical_levels(n, b),
+                "ns_per_barrier_level": metric_ms * 1e6 / args.steps / schedule.critical_levels(n, b)}
     # whole pass (SURVEY 8(d) B_pass): + 72 B per pair for the pair phase
     pass_bytes = metric_bytes + args.steps * 72 * (n * (n - 1) // 2)
     roofline["whole_pass"] = {"bytes_per_pass": pass_bytes / args.steps,

@@ -65,11 +65,14 @@ def tile_dram(tag):
     inst = sum(d["smsp__inst_executed.sum"][0] for d in per.values())
     return {"launches": n, "dram_read_bytes": rd, "dram_write_bytes": wr,
             "dram_bytes_per_launch": (rd + wr) / max(n, 1), "l2_bytes_per_launch": lts / max(n, 1),
+            "dram_bytes_per_pass": rd + wr, "l2_bytes_per_pass": lts,
             "duration_us_total": dur, "warp_instructions_total": inst}
 
 
-def full_summary(tag):
-    rep = os.path.join(OUT, f"prof_tile_{tag}.ncu-rep")
+def full_summary(tag, name="tile"):
+    rep = os.path.join(OUT, f"prof_{name}_{tag}.ncu-rep")
+    if not os.path.exists(rep):
+        return {}
     txt = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -77,7 +80,8 @@ def full_summary(tag):
     keep = ["Duration", "Elapsed Cycles", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate",
             "L2 Hit Rate", "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
             "Dynamic Shared Memory Per Block", "Block Size", "Grid Size", "Achieved Active Warps Per SM",
-            "Warp Cycles Per Issued Instruction", "Executed Instructions", "No Eligible"]
+            "Warp Cycles Per Issued Instruction", "Executed Instructions", "No Eligible",
+            "Eligible Warps Per Scheduler", "Achieved Occupancy"]
     out = {}
     for r in rows[1:]:
         d = dict(zip(hdr, r))
@@ -91,9 +95,15 @@ def main(tag, config=3):
     table, per, tot = launches(tag)
     dram = tile_dram(tag)
     full = full_summary(tag)
-    stall = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
-                            os.path.join(OUT, f"prof_tile_{tag}.ncu-rep"), "25"],
-                           capture_output=True, text=True).stdout
+    full_df = full_summary(tag, "df")
+
+    def stalls(name):
+        rep = os.path.join(OUT, f"prof_{name}_{tag}.ncu-rep")
+        if not os.path.exists(rep):
+            return ""
+        return subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, "25"],
+                              capture_output=True, text=True).stdout
+    stall, stall_df = stalls("tile"), stalls("df")
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write(f"# ncu summary, round {tag}\n\n")
         fh.write("## Launch list of `python bench.py --steps 3 --warmup 3 --no-cpu` "
@@ -101,13 +111,19 @@ def main(tag, config=3):
         fh.write(table + "\n\n")
         fh.write(f"## tile_round_kernel, every launch of pass 4 (config {config}, b=40): DRAM bytes\n\n")
         fh.write("```\n" + json.dumps(dram, indent=2) + "\n```\n\n")
-        fh.write("## Full capture (`--set full`), round NR/2 of pass 3 (tools/gpu_round.sh)\n\n```\n")
-        for k, v in full.items():
-            fh.write(f"{k:40s} {v}\n")
-        fh.write("```\n\n## Per-source-line instruction share and stall samples\n\n```\n" + stall + "```\n")
+        for title, f, st in (("a first-family round (round 10 of pass 3: hub rows in its longest tile)", full, stall),
+                             ("the dataflow launch of pass 3 (the second family)", full_df, stall_df)):
+            if not f:
+                continue
+            fh.write(f"## Full capture (`--set full`): {title}\n\n```\n")
+            for k, v in f.items():
+                fh.write(f"{k:40s} {v}\n")
+            fh.write("```\n\nPer-source-line instruction share and stall samples:\n\n```\n" + st + "```\n\n")
     path = os.path.join(PROF, "ncu_tile_kernel.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
-    data[f"config{config}_b40"] = {"dram_bytes_per_launch": dram["dram_bytes_per_launch"],
+    data[f"config{config}_b40"] = {"dram_bytes_per_pass": dram["dram_bytes_per_pass"],
+                                   "l2_bytes_per_pass": dram["l2_bytes_per_pass"],
+                                   "dram_bytes_per_launch": dram["dram_bytes_per_launch"],
                                    "l2_bytes_per_launch": dram["l2_bytes_per_launch"],
                                    "launches_measured": dram["launches"],
                                    "source": f"{tag}_ncu_summary.md"}
