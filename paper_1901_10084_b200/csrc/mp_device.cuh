@@ -161,6 +161,12 @@ struct TileArgs {
     int32_t wkp;                // WK row pitch in doubles (>= b; the TMA box width)
     int32_t wrp;                // WR row pitch in doubles (>= W)
     int32_t tma_store;          // interior WK blocks of the last band may be box-stored
+    // Row bands of a cluster: band d owns tile rows [bst[d], bst[d+1]) (uniform
+    // RB-row bands, or a split balancing the hub rows' exact steps), with
+    // blw[d] active lanes per warp slot row; rbmax = the most rows of a band.
+    uint8_t bst[17];
+    uint8_t blw[16];
+    int32_t rbmax;
     // Dataflow launch (df = 1): all tiles of the schedule's second family in
     // one launch; each cluster claims the next tile (qctr) and waits, ring
     // block by ring block, for the write-backs of the two tiles whose pairs it
@@ -249,7 +255,7 @@ struct CtaConst {
     unsigned long long *trace;
     StepConsts kc;
     int32_t b, nt, xsize;
-    int32_t C, band, RB;  // cluster size, this CTA's row band, rows per band
+    int32_t C, band, RB;  // cluster size, this CTA's row band, most rows of a band (WR staging)
     int32_t nwc;          // compute warps per CTA
     int32_t tl;           // MP_TIMELINE: this CTA records its timeline
     int32_t B32;          // shared address of the aligned staging base
@@ -259,7 +265,9 @@ struct CtaConst {
     uint32_t zero_lo;     // ... of the zero row (end of WK)
     uint32_t rk_lo;       // ... of RK
     uint32_t rk_row_mul;  // ceil(2^32 / (8b)): RK byte offset -> row (umulhi)
-    uint32_t band_mul;    // ceil(2^16 / RB): row -> band ((row * band_mul) >> 16)
+    uint8_t bst[17];      // band row starts (relative to ilo), bst[C] >= b
+    uint8_t blw[16];      // lanes per warp slot row of each band (full rows)
+    uint8_t rowband[64];  // tile row (relative) -> band
     const void *tmap;     // TMA descriptor of x (WK blocks), or null
     int32_t tma_st;       // the tile's K is b wide: interior WK blocks are stored by TMA
     int32_t wkp;          // WK row pitch (doubles)
@@ -296,7 +304,7 @@ __device__ __forceinline__ bool forward_jk(const CtaConst *cc, uint32_t ue, doub
         dlast = C - 1;
     } else if (ue >= cc->rk_lo) {
         const uint32_t row = __umulhi(ue - cc->rk_lo, cc->rk_row_mul);
-        dlast = min(C - 1, (int)((row * cc->band_mul) >> 16));
+        dlast = min(C - 1, (int)cc->rowband[row]);
     }
 #pragma unroll
     for (int d = 1; d < MP_CMAX; ++d)  // (unrolled to the largest cluster the host plans)
@@ -1520,11 +1528,14 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
     const int *loc_flag = &ts.done[warp > 0 ? warp - 1 : 0];
     int rem_warp = cc.nwc - 1;
     if (cc.colm) {
-        const int r0 = cc.band * cc.RB;
-        const int rbc = max(1, min(min(b, r0 + cc.RB), T.ihi - T.ilo + 1) - r0);  // the band's real rows
+        const int r0 = cc.bst[cc.band];
+        const int rbc = max(1, min(min(b, (int)cc.bst[cc.band + 1]), T.ihi - T.ilo + 1) - r0);  // the band's real rows
         const int qmax = min(warp * lwS + lwS - 1, rbc * b - 1);
         const int kmax = max(qmax, 0) / rbc;
-        rem_warp = min(cc.nwc - 1, (kmax * cc.RB + cc.RB - 1) / lwS);
+        if (cc.band > 0) {  // the previous band's slot of (its last row, column kmax)
+            const int rp = cc.bst[cc.band] - cc.bst[cc.band - 1];
+            rem_warp = min(cc.nwc - 1, (kmax * rp + rp - 1) / ((int)cc.blw[cc.band - 1] * S));
+        }
     }
     const bool has_rem = cc.band > 0 && (cc.colm || warp == 0);
     const uint32_t rem_flag = has_rem ? mapa(smem_u32(&ts.done[rem_warp]), cc.band - 1) : 0u;
@@ -1699,7 +1710,7 @@ __device__ __noinline__ void ring_producer(unsigned char *sm, const CtaConst *cc
     const int ptid = threadIdx.x - nwc * 32, pn = np * 32;
     double *smd = reinterpret_cast<double *>(sm);
     const int C = cc->C, band = cc->band;
-    const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
+    const int r0 = cc->bst[band], r1 = min(b, (int)cc->bst[band + 1]);
     const bool last_band = band == C - 1;
     double *WR = smd, *WK = smd + SmemMap<W>{b, cc->RB, cc->wkp, cc->wrp}.wk() / 8;
     const int xsize = cc->xsize;
@@ -1858,7 +1869,7 @@ __device__ __noinline__ void ring_producer_tma(unsigned char *sm, const CtaConst
     const int ptid = threadIdx.x - nwc * 32;
     double *smd = reinterpret_cast<double *>(sm);
     const int C = cc->C, band = cc->band;
-    const int r0 = band * cc->RB, r1 = min(b, r0 + cc->RB);
+    const int r0 = cc->bst[band], r1 = min(b, (int)cc->bst[band + 1]);
     const bool last_band = band == C - 1;
     double *WR = smd, *WK = smd + SmemMap<W>{b, cc->RB, cc->wkp, cc->wrp}.wk() / 8;
     const int blast = T.jhi / BLK;
@@ -1997,15 +2008,17 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
     }
     const TileDesc T = a.tiles[tidx];
     const int b = a.b;
-    const int RB = (b + C - 1) / C;
-    const int r0 = band * RB, r1 = min(b, r0 + RB);
+    const int RB = a.rbmax;  // most rows of a band (the WR staging)
+    const int r0 = a.bst[band], r1 = min(b, (int)a.bst[band + 1]);
     // Bands holding rows: all C, except for the first family's single-row
     // tiles (x = 1 - b: row 0 only), which run on band 0 alone -- the other
     // CTAs of the cluster only take part in its two barriers (no forwarding
     // to them, no lattice coupling; band 0 writes WK back).  The slot map of
     // a band covers its real rows (a single row's columns fill few warps).
     const int nrows = T.ihi - T.ilo + 1;
-    const int Ce = min(C, (nrows + RB - 1) / RB);
+    int Ce = 0;
+    for (int d = 0; d < C; ++d)
+        if ((int)a.bst[d] < nrows) Ce = d + 1;
     const bool idle_band = band >= Ce;
     const bool last_band = band == Ce - 1;
     const int64_t stream_base = T.stream0 + (int64_t)band * nwc;
@@ -2046,14 +2059,17 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
         cc.zero_lo = (uint32_t)B32 + (uint32_t)M.zero();
         cc.rk_lo = (uint32_t)B32 + (uint32_t)M.rk();
         cc.rk_row_mul = (uint32_t)((0x100000000ull + 8ull * (unsigned)b - 1) / (8ull * (unsigned)b));
-        cc.band_mul = (uint32_t)((65536u + (unsigned)RB - 1) / (unsigned)RB);
+        for (int d = 0; d <= C; ++d) cc.bst[d] = a.bst[d];
+        for (int d = 0; d < C; ++d) cc.blw[d] = a.blw[d];
+        for (int d = 0; d < C; ++d)
+            for (int r = a.bst[d]; r < min(b, (int)a.bst[d + 1]) && r < 64; ++r) cc.rowband[r] = (uint8_t)d;
         cc.tmap = tmap;
         cc.tma_st = a.tma_store && T.z - T.klo + 1 == b;
         cc.wkp = a.wkp;
         cc.wrp = a.wrp;
         cc.tl = a.trace != nullptr && a.round_id == a.tl_round && tidx == a.tl_tile && band < 8;
         cc.B32 = B32;
-        cc.lw = band_lanes(a.lw, nwc, S, max(1, min(r1, nrows) - r0), r1 - r0, b, a.colm != 0);
+        cc.lw = band_lanes(a.blw[band], nwc, S, max(1, min(r1, nrows) - r0), r1 - r0, b, a.colm != 0);
         cc.colm = a.colm;
         cc.tt = nullptr;
 #ifdef MP_TILETIME

@@ -16,6 +16,7 @@
 #include <nccl.h>  // types only: the functions are resolved at run time (nccl_api)
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -336,6 +337,7 @@ struct mp_handle {
     // max over rows of #{j : d_ij < 1/2} over its mean: hub rows (Chung-Lu
     // graphs) make the longest tiles of the small rounds exact-step bound
     double hub = 1.0;
+    std::vector<int32_t> deg;  // #{j : d_ij < 1/2} per row (hub band split)
 
     // device state (x and winvx dense n x ld; the rest packed C(n,2))
     double *x = nullptr, *winvx = nullptr;
@@ -351,6 +353,10 @@ struct mp_handle {
         int PR = 128;       // WR row pitch in doubles (>= W)
         bool colm = false;  // column-major slots in each band
         size_t smem = 0;
+        // row bands: band d owns tile rows [bst[d], bst[d+1]) with blw[d] lanes
+        // per warp slot row (uniform RB-row bands unless a split is given)
+        std::array<int, 17> bst{};
+        std::array<int, 16> blw{};
     };
     std::vector<RoundCfg> rcfg;       // per round
     // Dataflow launch of the schedule's second family (mp_device.cuh, DF_*):
@@ -617,11 +623,16 @@ double ring_waves(const mp_handle::RoundCfg &c, int b, int pitch, bool wk) {
 // with at most 15 compute warps (any S is correct: a warp waits until its
 // predecessor finished the whole batch), up to 3 producer warps, W = 256
 // ring when it fits.
-mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1) {
+mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
+                                const std::vector<int> *split = nullptr) {
     mp_handle::RoundCfg c;
     const int b = h->b;
     c.C = C;
     c.RB = (b + C - 1) / C;
+    if (split) {  // non-uniform bands: the WR staging holds the largest band
+        c.RB = 0;
+        for (int d = 0; d < C; ++d) c.RB = std::max(c.RB, (*split)[(size_t)d + 1] - (*split)[(size_t)d]);
+    }
     c.colm = C > 1;
     if (const char *e = getenv("MP_COLMAJOR")) c.colm = atoi(e) != 0;
     const int slots = c.RB * b;
@@ -650,6 +661,23 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1) {
     S = slots_per_thread(LW);
     c.S = S;
     c.NWC = (slots + LW * S - 1) / (LW * S);
+    for (int d = 0; d <= 16; ++d) c.bst[(size_t)d] = std::min(d * c.RB, b);
+    for (int d = 0; d < 16; ++d) c.blw[(size_t)d] = c.LW;
+    if (split) {
+        // every band's slots over the same warps, one slot per thread, its
+        // columns spread evenly (band_lanes); a band too big for that is refused
+        c.S = S = 1;
+        c.NWC = MAX_CTA_THREADS / 32 - 2;
+        if (const char *e = getenv("MP_HUB_NWC")) c.NWC = std::max(1, std::min(MAX_CTA_THREADS / 32 - 1, atoi(e)));
+        for (int d = 0; d <= C; ++d) c.bst[(size_t)d] = (*split)[(size_t)d];
+        for (int d = C + 1; d <= 16; ++d) c.bst[(size_t)d] = b;
+        for (int d = 0; d < C; ++d) {
+            const int rows = c.bst[(size_t)d + 1] - c.bst[(size_t)d];
+            c.blw[(size_t)d] = (rows * b + c.NWC - 1) / c.NWC;
+            if (rows < 1 || c.blw[(size_t)d] > 32) c.S = MAX_SLOTS + 1;
+        }
+        if (c.S > MAX_SLOTS) return c;
+    }
     c.NPW = std::min(3, MAX_CTA_THREADS / 32 - c.NWC);
     if (const char *e = getenv("MP_PRODUCERS")) c.NPW = std::max(1, std::min(MAX_CTA_THREADS / 32 - c.NWC, atoi(e)));
     c.NT = 32 * (c.NWC + c.NPW);
@@ -721,6 +749,45 @@ mp_handle::RoundCfg fallback_shape(const mp_handle *h, int cmax) {
     return none;
 }
 
+// Row bands of balanced weight: the fewest-weight maximum over C bands of at
+// most rmax rows each (binary search on the band weight, greedy bands), then
+// the bands with the most rows split until there are C.  Returns the C + 1
+// band starts, or an empty vector.
+std::vector<int> balanced_split(const std::vector<double> &w, int C, int rmax) {
+    const int b = (int)w.size();
+    if (C < 1 || b < C || rmax < 1 || (int64_t)rmax * C < b) return {};
+    auto greedy = [&](double T, std::vector<int> *out) {
+        int bands = 0, r = 0;
+        if (out) out->assign(1, 0);
+        while (r < b) {
+            double acc = 0.0;
+            int rows = 0;
+            while (r < b && rows < rmax && (rows == 0 || acc + w[(size_t)r] <= T)) acc += w[(size_t)r++], ++rows;
+            ++bands;
+            if (out) out->push_back(r);
+        }
+        return bands;
+    };
+    double lo = 0.0, hi = 0.0;
+    for (double v : w) lo = std::max(lo, v), hi += v;
+    for (int it = 0; it < 60; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (greedy(mid, nullptr) <= C) hi = mid;
+        else lo = mid;
+    }
+    std::vector<int> st;
+    if (greedy(hi, &st) > C) return {};
+    while ((int)st.size() - 1 < C) {
+        int best = -1;
+        for (int d = 0; d + 1 < (int)st.size(); ++d)
+            if (st[(size_t)d + 1] - st[(size_t)d] >= 2 && (best < 0 || st[(size_t)d + 1] - st[(size_t)d] > st[(size_t)best + 1] - st[(size_t)best]))
+                best = d;
+        if (best < 0) return {};
+        st.insert(st.begin() + best + 1, (st[(size_t)best] + st[(size_t)best + 1]) / 2);
+    }
+    return st;
+}
+
 // Launch shape per round: a round with few tiles spreads each tile over a
 // cluster of C SMs (row bands, mp_device.cuh), as large as the device can
 // co-schedule for all of the round's tiles at once (cnt[r] = tiles one
@@ -770,6 +837,31 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         if (const char *e = getenv("MP_HUB_LANES")) lw = std::max(1, std::min(32, atoi(e)));
         hub_shape = round_shape(h, C, lw);
         hubby = C > 1 && (C - 1) * RB < b && hub_shape.S <= MAX_SLOTS && hub_shape.smem <= 227 * 1024;
+        // Bands of balanced exact-step weight instead of RB rows each: the
+        // small rounds' critical tiles hold rows 1..b (row band 1), whose
+        // stored duals per row follow close-degree^1.5 (config 3, rows 1-3:
+        // 14.9 / 10.5 / 6.9 % measured, 14.4 / 10.2 / 6.8 % from degrees), so
+        // the hub rows get bands of their own (every tile of the launch uses
+        // the same relative split).
+        // (at most 6 rows a band keeps the W = 512 ring; measured, config 3:
+        // uniform 5-row bands 92.4 ms/pass; rmax 6 with 14 / 13 / 12 compute
+        // warps 83.3 / 86.4 / 86.1; rmax 7 or 8 (W = 256 then) 97.9 / 97.6)
+        int rmax = 6;
+        if (const char *e = getenv("MP_HUB_RMAX")) rmax = atoi(e);
+        if (hubby && rmax > 0 && (int64_t)h->deg.size() > b && !getenv("MP_NO_HUB_SPLIT")) {
+            std::vector<double> w((size_t)b);
+            for (int r = 0; r < b; ++r) w[(size_t)r] = std::pow((double)std::max(h->deg[(size_t)r + 1], 1), 1.5);
+            const std::vector<int> split = balanced_split(w, C, rmax);
+            if (!split.empty()) {
+                const mp_handle::RoundCfg sc = round_shape(h, C, lw, &split);
+                if (sc.S <= MAX_SLOTS && sc.smem <= 227 * 1024) hub_shape = sc;
+            }
+        }
+        if (hubby && getenv("MP_VERBOSE")) {
+            fprintf(stderr, "[mp] hub bands:");
+            for (int d = 0; d < C; ++d) fprintf(stderr, " [%d,%d) lw %d", hub_shape.bst[(size_t)d], hub_shape.bst[(size_t)d + 1], hub_shape.blw[(size_t)d]);
+            fprintf(stderr, " W=%d RB=%d smem=%zu\n", hub_shape.W, hub_shape.RB, hub_shape.smem);
+        }
     }
     std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
     std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
@@ -986,6 +1078,13 @@ const void *x_tmap(const mp_handle *h, int p) {
     return (p - h->b) % 2 == 0 && t >= 0 && t < 8 ? h->d_tmap[t] : nullptr;
 }
 
+// the launch's row bands (RoundCfg::bst / blw) into the kernel arguments
+void set_bands(TileArgs &ta, const mp_handle::RoundCfg &c) {
+    for (int d = 0; d <= 16; ++d) ta.bst[d] = (uint8_t)std::min(c.bst[(size_t)d], 255);
+    for (int d = 0; d < 16; ++d) ta.blw[d] = (uint8_t)c.blw[(size_t)d];
+    ta.rbmax = c.RB;
+}
+
 TileArgs tile_args(mp_handle *h) {
     TileArgs ta{};
     ta.x = h->x;
@@ -1057,6 +1156,7 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
         ta.wrp = c.PR;
         ta.tmap = x_tmap(h, c.P);
         ta.tma_store = h->tma_store;
+        set_bands(ta, c);
         ta.df = 1;
         ta.dep = h->d_dep;
         ta.prog = h->d_prog;
@@ -1078,6 +1178,7 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
     ta.wrp = c.PR;
     ta.tmap = x_tmap(h, c.P);
     ta.tma_store = h->tma_store;
+    set_bands(ta, c);
     return launch_tiles(h, c, ta, (int)cnt);
 }
 
@@ -1249,9 +1350,9 @@ Decoded decode_entry(const mp_handle *h, int64_t t, int w, uint32_t key) {
     const int lane = r2 / 3, kind = r2 % 3;
     // a band's slot map covers its real rows (single-row tiles: band 0, 1 row)
     const int64_t nrows = (int64_t)T.ihi - T.ilo + 1;
-    const int64_t r0 = (int64_t)band * c.RB, r1 = std::min<int64_t>(h->b, r0 + c.RB),
+    const int64_t r0 = c.bst[(size_t)band], r1 = std::min<int64_t>(h->b, c.bst[(size_t)band + 1]),
                   rbc = std::max<int64_t>(1, std::min<int64_t>(r1, nrows) - r0);
-    const int64_t LW = band_lanes(c.LW, c.NWC, c.S, (int)rbc, (int)(r1 - r0), h->b, c.colm);
+    const int64_t LW = band_lanes(c.blw[(size_t)band], c.NWC, c.S, (int)rbc, (int)(r1 - r0), h->b, c.colm);
     const int64_t q = ((int64_t)wb * c.S + s) * LW + lane;
     const int64_t ii = c.colm ? r0 + q % rbc : r0 + q / h->b;
     const int64_t kk = c.colm ? q / rbc : q % h->b;
@@ -1378,6 +1479,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         for (int32_t v : deg) sum += v, mx = std::max(mx, v);
         const double mean = (double)sum / (double)n;
         h->hub = mx / std::max(mean, 1.0);
+        h->deg = deg;
         if (getenv("MP_VERBOSE")) fprintf(stderr, "[mp] hub factor %.1f (max degree %d, mean %.1f)\n", h->hub, mx, mean);
     }
 
@@ -1858,12 +1960,14 @@ int mp_set_duals(mp_handle *h, int64_t nnz, const int64_t *keys, const double *v
         if (h->sh.on && h->sh.owner[(size_t)t] != h->sh.rank) continue;  // another shard's dual
         const TileDesc &T = h->tiles[(size_t)t];
         const mp_handle::RoundCfg &c = h->rcfg[(size_t)h->tile_round[(size_t)t]];
-        const int64_t band = (i - T.ilo) / c.RB, S = c.S;
+        int64_t band = 0;
+        while (band + 1 < c.C && c.bst[(size_t)band + 1] <= i - T.ilo) ++band;
+        const int64_t S = c.S;
         const int64_t nrows = (int64_t)T.ihi - T.ilo + 1;
-        const int64_t r0 = band * c.RB, r1 = std::min<int64_t>(b, r0 + c.RB),
+        const int64_t r0 = c.bst[(size_t)band], r1 = std::min<int64_t>(b, c.bst[(size_t)band + 1]),
                       rbc = std::max<int64_t>(1, std::min<int64_t>(r1, nrows) - r0);
         const int64_t q = c.colm ? (k - T.klo) * rbc + (i - T.ilo - r0) : (i - T.ilo - r0) * b + (k - T.klo);
-        const int64_t LW = band_lanes(c.LW, c.NWC, c.S, (int)rbc, (int)(r1 - r0), (int)b, c.colm);
+        const int64_t LW = band_lanes(c.blw[(size_t)band], c.NWC, c.S, (int)rbc, (int)(r1 - r0), (int)b, c.colm);
         const int64_t w = q / (LW * S), s = (q % (LW * S)) / LW, lane = q % LW;
         const int64_t lvl = i + j + k - T.Lbeg;
         const uint32_t key32 = (uint32_t)(((lvl * S + s) * 96) + lane * 3 + kind);
