@@ -372,6 +372,7 @@ def run_gpu(args):
         tt = torch.tensor([t_dev, metric_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_dev, metric_ms = float(tt[0]), float(tt[1])
+    xchg = sess.exchange_volume() if args.sharded else (0, 0)
     sess.close()
     value = copies * args.steps * rows / t_dev
 
@@ -393,6 +394,11 @@ def run_gpu(args):
                 "launches_per_pass": launches / max(args.steps, 1),
                 "barrier_levels_per_pass": schedule.critical_levels(n, b),
                 "ns_per_barrier_level": metric_ms * 1e6 / args.steps / schedule.critical_levels(n, b)}
+    if args.sharded:  # NVLink exchange of this rank (not part of B_pass)
+        roofline["exchange"] = {"scheme": "footprint blocks to the next toucher's rank (grouped send/recv)",
+                                "sent_bytes_per_pass_rank": 8 * xchg[0],
+                                "received_bytes_per_pass_rank": 8 * xchg[1],
+                                "all_gather_bytes_per_pass_rank": 8 * tx * (ws - 1) / ws}
     # whole pass (SURVEY 8(d) B_pass): + 72 B per pair for the pair phase
     pass_bytes = metric_bytes + args.steps * 72 * (n * (n - 1) // 2)
     roofline["whole_pass"] = {"bytes_per_pass": pass_bytes / args.steps,

@@ -145,11 +145,13 @@ int mp_get_duals_ranked(mp_handle *h, int64_t *keys, double *vals, int64_t *orde
  * Replaces the reference's worker threads (solver._worker_pass,
  * solver.py:116-163; round ownership Round.worker_of, schedule.py:79-80) with
  * one process per GPU.  The tiles of each round are assigned to ranks by
- * longest-processing-time (mp_shard_plan); a rank keeps the whole x, runs its
- * tiles, keeps their duals, and after every round exchanges the pairs its
- * tiles wrote (NCCL all-gather on the session stream), so every rank follows
- * the single-GPU trajectory bit for bit.  Counters (nnz, max violation) are
- * all-reduced, so every rank reports the global PassStats. */
+ * longest-processing-time (mp_shard_plan); a rank keeps a whole x, runs its
+ * tiles, keeps their duals, and after every round sends each b x b block its
+ * tiles wrote to the rank whose tile touches that block next (grouped NCCL
+ * send/recv on the session stream; a block's last toucher of the pass sends it
+ * to every rank), so every tile reads what a single GPU would hold and every
+ * rank follows the single-GPU trajectory bit for bit.  Counters (nnz, max
+ * violation) are all-reduced, so every rank reports the global PassStats. */
 
 /* Tile owners of the LPT plan, in schedule order (host only, no device).
  * owner may be NULL to query the tile count. */
@@ -165,6 +167,15 @@ int mp_nccl_unique_id(void *id);
  * sessions of one process driven together by mp_group_run_passes (exchange by
  * device copies; a test transport that shares the exact per-round code). */
 int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id);
+
+/* Values (8 bytes each, padding included) this rank sends and receives per
+ * pass under the exchange plan of mp_shard (0 for an unsharded session). */
+int mp_shard_volume(mp_handle *h, int64_t *sent, int64_t *received);
+
+/* The exchange plan of a `world`-way sharded solve (host only, no device):
+ * vol[(r * world + src) * world + dst] = pairs rank src sends to rank dst
+ * after round r.  vol may be NULL to query the round count. */
+int mp_shard_route(int64_t n, int32_t b, int32_t world, int64_t *vol, int64_t *nrounds);
 
 /* Run npasses over a local group (hs[0..world) = the local shards, any order);
  * out[] receives the (global) stats, identical on every member. */

@@ -41,27 +41,64 @@ def sources():
                   if f.endswith((".cu", ".cuh", ".h", ".cpp")))
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
-    """Compile csrc/ into _lib/libmetricproj_b200.so (sm_100a).  A named
-    ``variant`` with extra ``defines`` (e.g. MP_TRACE) builds a side library
-    for diagnostics, selected at load time with MP_LIB_VARIANT."""
-    os.makedirs(LIB_DIR, exist_ok=True)
-    out = LIB_PATH if not variant else os.path.join(LIB_DIR, f"libmetricproj_b200_{variant}.so")
-    deps = sources() + [os.path.join(INCLUDE, "metricproj_b200.h")]
-    if (not force and os.path.exists(out)
-            and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in deps)):
-        return out
+KNOBS_VARIANT = "knobs"  # the product library + the experiment switches (-DMP_KNOBS)
+
+
+def lib_path(variant: str = "") -> str:
+    return LIB_PATH if not variant else os.path.join(LIB_DIR, f"libmetricproj_b200_{variant}.so")
+
+
+def _build_cmd(out, defines):
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
-    tmp = out + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-I", CSRC,
-           "-o", tmp, os.path.join(CSRC, "mp_solver.cu"), "-ldl"]
+    return [nvcc, *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-I", CSRC,
+            "-o", out + ".tmp", os.path.join(CSRC, "mp_solver.cu"), "-ldl"]
+
+
+def _stale(out, force):
+    deps = sources() + [os.path.join(INCLUDE, "metricproj_b200.h")]
+    return (force or not os.path.exists(out)
+            or os.path.getmtime(out) < max(os.path.getmtime(p) for p in deps))
+
+
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Compile csrc/ into _lib/libmetricproj_b200.so (sm_100a).  A named
+    ``variant`` with extra ``defines`` (e.g. MP_TRACE) builds a side library
+    for diagnostics, selected at load time with MP_LIB_VARIANT or
+    ``use_variant``; every variant also gets -DMP_KNOBS (the experiment
+    switches the product library does not have)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    out = lib_path(variant)
+    if not _stale(out, force):
+        return out
+    if variant:
+        defines = tuple(dict.fromkeys(("MP_KNOBS", *defines)))
+    cmd = _build_cmd(out, defines)
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, out)
+    os.replace(out + ".tmp", out)
     return out
+
+
+def build_all(force: bool = False, verbose: bool = False):
+    """The product library and the ``knobs`` variant (shape-forcing tests),
+    compiled side by side."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    jobs = []
+    for variant, defines in (("", ()), (KNOBS_VARIANT, ("MP_KNOBS",))):
+        out = lib_path(variant)
+        if _stale(out, force):
+            cmd = _build_cmd(out, defines)
+            if verbose:
+                print(" ".join(cmd))
+            jobs.append((out, subprocess.Popen(cmd)))
+    for out, proc in jobs:
+        if proc.wait() != 0:
+            raise subprocess.CalledProcessError(proc.returncode, "nvcc")
+        os.replace(out + ".tmp", out)
+    return [lib_path(""), lib_path(KNOBS_VARIANT)]
 
 
 class MPInstance(ctypes.Structure):
@@ -96,25 +133,43 @@ EXPORTS = ("mp_create", "mp_run_passes", "mp_get_state", "mp_set_state", "mp_dua
            "mp_get_duals", "mp_set_duals", "mp_state_max_violation", "mp_get_timing",
            "mp_trace", "mp_flush_l2", "mp_destroy", "mp_max_violation", "mp_check_division",
            "mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
-           "mp_group_run_passes", "mp_cc_instance", "mp_accumulate_aty", "mp_dykstra_steps",
+           "mp_shard_volume", "mp_shard_route", "mp_group_run_passes", "mp_cc_instance", "mp_accumulate_aty", "mp_dykstra_steps",
            "mp_last_error", "mp_version")
 
-_lib = None
+_libs = {}                                        # variant -> loaded library
+_variant = os.environ.get("MP_LIB_VARIANT", "")   # the variant load() returns
+
+
+class use_variant:
+    """``with use_variant("knobs"):`` -- every call inside goes to that library
+    variant (sessions must be created and closed inside the block)."""
+
+    def __init__(self, variant):
+        self.variant = variant
+
+    def __enter__(self):
+        global _variant
+        self.prev, _variant = _variant, self.variant
+        return self
+
+    def __exit__(self, *exc):
+        global _variant
+        _variant = self.prev
+        return False
 
 
 def load():
     """Load the shared library (raises if it has not been built)."""
-    global _lib
-    if _lib is not None:
-        return _lib
-    variant = os.environ.get("MP_LIB_VARIANT", "")
-    path = LIB_PATH if not variant else os.path.join(LIB_DIR, f"libmetricproj_b200_{variant}.so")
+    variant = _variant
+    if variant in _libs:
+        return _libs[variant]
+    path = lib_path(variant)
     if not os.path.exists(path):
         raise ImportError(
-            f"{path} is missing: run paper_1901_10084_b200._native.build() "
+            f"{path} is missing: run paper_1901_10084_b200._native.build_all() "
             "(or __graft_entry__.build()); there is no CPU fallback")
     L = ctypes.CDLL(path)
-    if variant:  # a diagnostic build may predate some entry points
+    if variant and variant != KNOBS_VARIANT:  # a diagnostic build may predate some entry points
         class _Tolerant:
             def __init__(self, lib):
                 self.__dict__["_lib"] = lib
@@ -157,6 +212,8 @@ def load():
                                 ctypes.POINTER(ctypes.c_int32), I]
     L.mp_nccl_unique_id.argtypes = [ctypes.c_char_p]
     L.mp_shard.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p]
+    L.mp_shard_volume.argtypes = [P, I, I]
+    L.mp_shard_route.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, I, I]
     L.mp_group_run_passes.argtypes = [ctypes.POINTER(P), ctypes.c_int32, ctypes.c_int32,
                                       ctypes.POINTER(MPPassStats)]
     L.mp_cc_instance.argtypes = [ctypes.c_int64, I, ctypes.POINTER(ctypes.c_int32), ctypes.c_double,
@@ -165,6 +222,7 @@ def load():
                                    ctypes.c_double, ctypes.c_int64, D, D,
                                    ctypes.POINTER(ctypes.c_int32)]
     for name in ("mp_get_duals_ranked", "mp_shard_plan", "mp_nccl_unique_id", "mp_shard",
+                 "mp_shard_volume", "mp_shard_route",
                  "mp_group_run_passes", "mp_cc_instance", "mp_dykstra_steps"):
         getattr(L, name).restype = ctypes.c_int
     L.mp_last_error.restype = ctypes.c_char_p
@@ -173,7 +231,7 @@ def load():
                  "mp_set_duals", "mp_state_max_violation", "mp_get_timing", "mp_flush_l2",
                  "mp_max_violation"):
         getattr(L, name).restype = ctypes.c_int
-    _lib = L
+    _libs[variant] = L
     return L
 
 

@@ -3,20 +3,27 @@
 // The tiles of a round are pairwise conflict-free (schedule.py:235-250), so
 // a round's tiles are spread over the ranks (longest-processing-time per
 // round, distributed.shard_rounds) and each tile always runs on the same rank,
-// which therefore keeps its duals.  Every rank holds the whole
-// x.  After each round a rank publishes the *footprint* of each of its tiles
-// -- exactly the pairs the tile kernel writes back (ring_block / rk_block
-// predicates in mp_device.cuh) -- and every rank applies the other ranks'
-// footprints, so before round r+1 all ranks hold the x a single GPU would.
-// Footprints of one round are disjoint, so the order of application does not
-// matter and the result is bitwise the single-GPU trajectory.
+// which therefore keeps its duals.  Every rank holds a whole
+// x, but between the pair phases only the blocks a rank is about to touch are
+// kept current: tiles and pairs live on one grid of b x b blocks (row block I
+// = rows [1 + (I-1) b, I b], column block K = columns [n - b - K b, n - 1 -
+// K b]), a tile's footprint -- exactly the pairs the tile kernel writes back
+// (ring_block / rk_block predicates in mp_device.cuh) -- is a union of whole
+// grid blocks, and the tiles touching one block form a fixed sequence in
+// schedule order (distributed.block_touchers).  After each round a rank sends
+// every block of its tiles' footprints to the rank of the block's *next
+// toucher* only (distributed.next_toucher; nothing when that is the same
+// rank), and a block's last toucher of the pass sends it to every rank, so
+// all ranks enter the pair phase with the single-GPU x.  A tile thus reads
+// exactly what a single GPU would have in x, and the trajectory is bitwise
+// the single-GPU one.  Per rank that is ~(G-1)/G^2 of the touched pairs per
+// pass instead of the (G-1)/G an all-gather of every footprint moves.
 //
-// Footprint layout (padded, coalesced; `count` values per tile):
-//   WR part  b rows i = ilo+ii      x wrw columns j = wr0 + c  (x_ij, j < klo)
-//   RK part  b rows i = ilo+ii      x b   columns k = klo + kk (x_ik)
-//   WK part  nwk rows j = wk0 + jj  x b   columns k = klo + kk (x_jk, j > ihi)
-// Slots outside the tile's pairs (i >= j, k > z, ...) are padding: packed as
-// garbage, never unpacked.
+// A piece is a rectangle of x (rows [row0, row0 + nrows) x columns [col0,
+// col0 + ncols)), row-major in the exchange buffer at `off`; only the pairs
+// row < col are copied (the rest is padding, never unpacked).  Consecutive
+// blocks of one footprint part with one destination are merged and pieces of
+// more than PIECE_MAX values split, identically on both sides.
 #pragma once
 
 #include <cstdint>
@@ -25,60 +32,24 @@
 
 namespace mp {
 
-struct FootDesc {
-    TileDesc t;
-    int64_t off;    // offset of this footprint in its owner's round buffer
-    int32_t wr0;    // first WR column: max(jlo, ilo+1)
-    int32_t wrw;    // WR row width: max(0, min(jhi, klo-1) - wr0 + 1)
-    int32_t wk0;    // first WK row: max(jlo, ihi+1)
-    int32_t nwk;    // WK rows: max(0, jhi - wk0 + 1)
-    int32_t owner;  // rank that runs the tile
-    int32_t pad;
+struct PieceDesc {
+    int32_t row0, nrows, col0, ncols;
+    int64_t off;  // offset in the rank's send (pack) or receive (unpack) buffer
 };
 
-__host__ __device__ inline int64_t foot_count(const FootDesc &f, int b) {
-    return (int64_t)b * f.wrw + (int64_t)b * b + (int64_t)f.nwk * b;
-}
+constexpr int64_t PIECE_MAX = 1 << 16;  // values per piece (one CTA each)
 
-// Element e of a footprint -> (row, col) and whether it is one of the tile's
-// write-back pairs.
-__device__ __forceinline__ bool foot_elem(const FootDesc &f, int b, int64_t e, int &row, int &col) {
-    const TileDesc &T = f.t;
-    const int64_t nwr = (int64_t)b * f.wrw;
-    if (e < nwr) {
-        const int ii = (int)(e / f.wrw);
-        row = T.ilo + ii;
-        col = f.wr0 + (int)(e - (int64_t)ii * f.wrw);
-        return row <= T.ihi && col >= T.jlo && col <= T.jhi && col < T.klo && row < col;
-    }
-    e -= nwr;
-    if (e < (int64_t)b * b) {
-        const int ii = (int)(e / b);
-        row = T.ilo + ii;
-        col = T.klo + (int)(e - (int64_t)ii * b);
-        return row <= T.ihi && col <= T.z && row < col;
-    }
-    e -= (int64_t)b * b;
-    const int jj = (int)(e / b);
-    row = f.wk0 + jj;
-    col = T.klo + (int)(e - (int64_t)jj * b);
-    return jj < f.nwk && col <= T.z && row < col;
-}
-
-// PACK: copy the footprints of `rank`'s tiles from x into buf (its round
-// buffer).  !PACK: write the footprints of every other rank's tiles from
-// buf + owner*stride into x.  One CTA per tile of the round.
+// PACK: x -> buf.  !PACK: buf -> x.  One CTA per piece.
 template <bool PACK>
-__global__ void __launch_bounds__(256) foot_copy_kernel(const FootDesc *fd, double *x, int64_t ld,
-                                                        int b, double *buf, int64_t stride,
-                                                        int rank) {
-    const FootDesc f = fd[blockIdx.x];
-    if (PACK ? f.owner != rank : f.owner == rank) return;
-    double *base = buf + (PACK ? 0 : (int64_t)f.owner * stride) + f.off;
-    const int64_t cnt = foot_count(f, b);
-    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-        int row, col;
-        if (!foot_elem(f, b, e, row, col)) continue;
+__global__ void __launch_bounds__(256) piece_copy_kernel(const PieceDesc *pd, double *x, int64_t ld,
+                                                         double *buf) {
+    const PieceDesc p = pd[blockIdx.x];
+    double *base = buf + p.off;
+    const int cnt = p.nrows * p.ncols;  // <= PIECE_MAX
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const int r = e / p.ncols, c = e - r * p.ncols;
+        const int row = p.row0 + r, col = p.col0 + c;
+        if (row >= col) continue;
         double *gp = x + (int64_t)row * ld + col;
         if (PACK) base[e] = *gp;
         else *gp = base[e];

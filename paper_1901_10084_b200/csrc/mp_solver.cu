@@ -42,6 +42,21 @@ namespace {
 
 thread_local std::string g_err;
 
+// Experiment switches (launch-shape overrides such as MP_CLUSTER / MP_FORCE_C /
+// MP_NO_TMA, the forced pool overflow MP_POOL_CAP0, timing toggles) exist only
+// in -DMP_KNOBS builds: the `knobs` library variant that the shape-forcing
+// tests and the tools/ A/B scripts load, and the diagnostic variants.  The
+// product library reads two environment variables only: MP_NCCL_LIB (path of
+// the NCCL library to dlopen) and MP_VERBOSE (planner log on stderr).
+inline const char *knob(const char *name) {
+#ifdef MP_KNOBS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 int fail(int code, const char *fmt, ...) {
     char buf[512];
     va_list ap;
@@ -278,6 +293,62 @@ void lpt_owner(int64_t b, int world, const std::vector<int64_t> &tx, const std::
     }
 }
 
+// The tile that touches grid block (Ia, Kb) next after tile (I, K) in a pass
+// (distributed.next_toucher; tests/test_distributed.py checks the closed form
+// against the per-pair last toucher of the whole schedule).  Blocks and tiles
+// share one grid: row block I = rows [1 + (I-1) b, I b] (0: row 0), column
+// block K = columns [n - b - K b, n - 1 - K b].  The touchers of (Ia, Kb), in
+// schedule order, are for Kb >= Ia the tiles (Ia, Ia..Kb), (Ia-1..0, Kb),
+// (Ia, Ia-1..0), else (Kb..0, Kb), (Kb+1..Ia, Kb), (Ia, Kb-1..0); only the
+// block's own tile (Ia, Kb) can be missing from the schedule.  Returns false
+// when (I, K) is the block's last toucher of the pass.
+template <class Exists>
+bool next_toucher(int64_t Ia, int64_t Kb, int64_t I, int64_t K, Exists exists, int64_t &nI, int64_t &nK) {
+    auto first = [&](int64_t i0, int64_t k0, bool have1, int64_t i1, int64_t k1) {
+        if (exists(i0, k0)) {
+            nI = i0, nK = k0;
+            return true;
+        }
+        if (have1 && exists(i1, k1)) {
+            nI = i1, nK = k1;
+            return true;
+        }
+        return false;
+    };
+    const int64_t tail = Kb >= Ia ? Ia : Kb;  // the closing run (Ia, tail-1 .. 0) of the row
+    if (I == Ia && K < tail) {
+        if (K < 1) return false;
+        nI = Ia, nK = K - 1;
+        return true;
+    }
+    if (Kb >= Ia) {
+        if (I == Ia) {  // opening run of the row, K in [Ia, Kb]
+            if (K < Kb) return first(Ia, K + 1, Ia >= 1, Ia - 1, Kb);
+            if (Ia < 1) return false;
+            nI = Ia - 1, nK = Kb;
+            return true;
+        }
+        if (I >= 1) {  // column run, I falling from Ia - 1 to 0
+            nI = I - 1, nK = Kb;
+            return true;
+        }
+        if (Ia < 1) return false;
+        nI = Ia, nK = Ia - 1;
+        return true;
+    }
+    if (I <= Kb && K == Kb) {  // column run of the first family, I falling
+        if (I >= 1) {
+            nI = I - 1, nK = Kb;
+            return true;
+        }
+        return first(Kb + 1, Kb, Kb >= 1, Ia, Kb - 1);
+    }
+    if (K == Kb && I < Ia) return first(I + 1, Kb, Kb >= 1, Ia, Kb - 1);  // second family, I rising
+    if (Kb < 1) return false;  // the block's own tile
+    nI = Ia, nK = Kb - 1;
+    return true;
+}
+
 // NCCL, resolved at run time so the library loads (and the CPU tests run)
 // without it: prefer the copy already in the process (torch's), then
 // $MP_NCCL_LIB, then the system libnccl.so.2.
@@ -285,8 +356,8 @@ struct NcclApi {
     ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
-                              cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
                               ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
@@ -308,12 +379,13 @@ const NcclApi &nccl_api() {
         a.getUniqueId = (decltype(a.getUniqueId))dlsym(lib, "ncclGetUniqueId");
         a.commInitRank = (decltype(a.commInitRank))dlsym(lib, "ncclCommInitRank");
         a.commDestroy = (decltype(a.commDestroy))dlsym(lib, "ncclCommDestroy");
-        a.allGather = (decltype(a.allGather))dlsym(lib, "ncclAllGather");
+        a.send = (decltype(a.send))dlsym(lib, "ncclSend");
+        a.recv = (decltype(a.recv))dlsym(lib, "ncclRecv");
         a.allReduce = (decltype(a.allReduce))dlsym(lib, "ncclAllReduce");
         a.groupStart = (decltype(a.groupStart))dlsym(lib, "ncclGroupStart");
         a.groupEnd = (decltype(a.groupEnd))dlsym(lib, "ncclGroupEnd");
         a.errorString = (decltype(a.errorString))dlsym(lib, "ncclGetErrorString");
-        if (!a.getUniqueId || !a.commInitRank || !a.commDestroy || !a.allGather || !a.allReduce ||
+        if (!a.getUniqueId || !a.commInitRank || !a.commDestroy || !a.send || !a.recv || !a.allReduce ||
             !a.groupStart || !a.groupEnd || !a.errorString) {
             a.why = "libnccl.so.2 lacks a required symbol";
             a.getUniqueId = nullptr;
@@ -414,9 +486,15 @@ struct mp_handle {
         ncclComm_t comm = nullptr;
         std::vector<int32_t> owner;               // per tile
         std::vector<int64_t> my_off, my_cnt;      // per round, into d_my_tiles
-        std::vector<int64_t> round_max;           // per round: max footprint values over ranks
+        // next-toucher exchange (mp_shard.cuh): per round the pieces this rank
+        // packs (grouped by destination) and unpacks (grouped by source), and
+        // the values per peer segment of its send / receive buffer
+        std::vector<int64_t> sp_off, sp_cnt, rp_off, rp_cnt;  // per round, into d_send_pc / d_recv_pc
+        std::vector<int64_t> scnt, soff, rcnt, roff;          // per round x peer
+        std::vector<char> round_any;                          // any rank sends anything after round r
+        int64_t sent_per_pass = 0, recv_per_pass = 0;         // values (8 bytes each)
         TileDesc *d_my_tiles = nullptr;
-        FootDesc *d_foot = nullptr;               // per tile, schedule order
+        PieceDesc *d_send_pc = nullptr, *d_recv_pc = nullptr;
         double *sendbuf = nullptr, *recvbuf = nullptr;
         PassCounters *d_local = nullptr, *h_local = nullptr;  // this rank's counters
         int64_t local_nnz = 0;
@@ -446,7 +524,8 @@ struct mp_handle {
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
         cudaFree(sh.d_my_tiles);
-        cudaFree(sh.d_foot);
+        cudaFree(sh.d_send_pc);
+        cudaFree(sh.d_recv_pc);
         cudaFree(sh.sendbuf);
         cudaFree(sh.recvbuf);
         cudaFree(sh.d_local);
@@ -512,7 +591,7 @@ cudaLaunchConfig_t tile_launch_config(const mp_handle::RoundCfg &c, int ntiles, 
         attr[na].val.clusterDim.z = 1;
         ++na;
     }
-    if (!getenv("MP_NO_PDL")) {  // programmatic dependent launch of consecutive rounds
+    if (!knob("MP_NO_PDL")) {  // programmatic dependent launch of consecutive rounds
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -583,7 +662,7 @@ int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
 // WK blocks can move as 2-D TMA boxes (tiled schedule, even b: box rows of
 // b * 8 bytes, a multiple of 16)
 bool tma_possible(const mp_handle *h) {
-    return h->kind == 2 && !(h->b & 1) && h->b + 2 <= 256 && !getenv("MP_NO_TMA");
+    return h->kind == 2 && !(h->b & 1) && h->b + 2 <= 256 && !knob("MP_NO_TMA");
 }
 
 // Shared-memory wavefronts per warp-wide 8-byte ring load (x_ij from WR
@@ -634,10 +713,10 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
         for (int d = 0; d < C; ++d) c.RB = std::max(c.RB, (*split)[(size_t)d + 1] - (*split)[(size_t)d]);
     }
     c.colm = C > 1;
-    if (const char *e = getenv("MP_COLMAJOR")) c.colm = atoi(e) != 0;
+    if (const char *e = knob("MP_COLMAJOR")) c.colm = atoi(e) != 0;
     const int slots = c.RB * b;
     int S = 1;
-    if (const char *e = getenv("MP_SLOTS")) S = std::max(S, atoi(e));
+    if (const char *e = knob("MP_SLOTS")) S = std::max(S, atoi(e));
     // Column-major bands: a warp holds whole columns (LW a multiple of RB).  A
     // column split over two warps couples them through the in-column lattice
     // dependency and every exact step of the column stalls both (config 2, RB
@@ -655,7 +734,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
         if (s <= slots_per_thread(32) && (slots + lw * s - 1) / (lw * s) <= MAX_CTA_THREADS / 32 - 3) c.LW = lw;
     }
     if (lanes < 0)
-        if (const char *e = getenv("MP_LANES")) lanes = atoi(e);
+        if (const char *e = knob("MP_LANES")) lanes = atoi(e);
     if (lanes > 0 && C > 1) c.LW = std::max(1, std::min(32, lanes));  // cluster rounds only (one CTA needs them all)
     const int LW = c.LW;
     S = slots_per_thread(LW);
@@ -668,7 +747,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
         // columns spread evenly (band_lanes); a band too big for that is refused
         c.S = S = 1;
         c.NWC = MAX_CTA_THREADS / 32 - 2;
-        if (const char *e = getenv("MP_HUB_NWC")) c.NWC = std::max(1, std::min(MAX_CTA_THREADS / 32 - 1, atoi(e)));
+        if (const char *e = knob("MP_HUB_NWC")) c.NWC = std::max(1, std::min(MAX_CTA_THREADS / 32 - 1, atoi(e)));
         for (int d = 0; d <= C; ++d) c.bst[(size_t)d] = (*split)[(size_t)d];
         for (int d = C + 1; d <= 16; ++d) c.bst[(size_t)d] = b;
         for (int d = 0; d < C; ++d) {
@@ -679,7 +758,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
         if (c.S > MAX_SLOTS) return c;
     }
     c.NPW = std::min(3, MAX_CTA_THREADS / 32 - c.NWC);
-    if (const char *e = getenv("MP_PRODUCERS")) c.NPW = std::max(1, std::min(MAX_CTA_THREADS / 32 - c.NWC, atoi(e)));
+    if (const char *e = knob("MP_PRODUCERS")) c.NPW = std::max(1, std::min(MAX_CTA_THREADS / 32 - c.NWC, atoi(e)));
     c.NT = 32 * (c.NWC + c.NPW);
     // ring width: as many j-slots as fit (a cluster's bands drift apart by up
     // to a few hundred levels; the ring bounds that drift)
@@ -689,7 +768,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
     c.W = 128;
     if (h->unit_x && fits(256, b, 256)) c.W = 256;
     if (h->unit_x && C > 1 && S <= 2 && fits(512, b, 512)) c.W = 512;
-    if (const char *e = getenv("MP_RING_W")) c.W = std::min(c.W, std::max(128, atoi(e)));
+    if (const char *e = knob("MP_RING_W")) c.W = std::min(c.W, std::max(128, atoi(e)));
     // Progress needs the ring to hold the slowest warp's whole j-window: the
     // producer frees blocks below slow - ihi - z and the warp reads up to
     // slow - ilo - klo, a span of 2b - 2, plus the block being loaded.  (b <=
@@ -707,7 +786,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
     // aligned; a WK pitch > b is loaded as a wider TMA box and written back
     // element-wise).
     c.PR = c.W;
-    if (!getenv("MP_WR_PITCH_W")) {
+    if (!knob("MP_WR_PITCH_W")) {
         double best = 1e30;
         for (int pr = c.W; pr <= c.W + 14; pr += 2) {
             const double v = ring_waves(c, b, pr, false);
@@ -715,7 +794,7 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
         }
     }
     c.P = b;
-    if (!getenv("MP_WK_PITCH_B")) {
+    if (!knob("MP_WK_PITCH_B")) {
         const int step = (b & 1) ? 1 : 2;
         const double plain = ring_waves(c, b, b, true);
         double best = 1e30;
@@ -800,11 +879,11 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int cmax = MP_CMAX;
-    if (const char *e = getenv("MP_CLUSTER")) cmax = std::max(1, std::min(MP_CMAX, atoi(e)));
+    if (const char *e = knob("MP_CLUSTER")) cmax = std::max(1, std::min(MP_CMAX, atoi(e)));
     const mp_handle::RoundCfg one = fallback_shape(h, cmax);
     if (one.C == 0) return fail(MP_ERR_UNSUPPORTED, "tile size %d does not fit the device's launch shapes", b);
     int fb = 2;  // cluster size for rounds whose clusters do not all fit at once
-    if (const char *e = getenv("MP_WAVE_C")) fb = atoi(e);
+    if (const char *e = knob("MP_WAVE_C")) fb = atoi(e);
     fb = std::min(fb, cmax);
     // Rounds of up to minc_cnt tiles get at least minc CTAs per tile, in waves
     // if need be: the longest tiles go first and their time is the round's
@@ -812,21 +891,21 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     // tiles) 167 -> 123 ms; config 4 (uniform) 586 -> 592 ms; config 5 -1%.
     // Larger rounds are throughput-bound and keep the largest fitting C.
     int minc = 6;
-    if (const char *e = getenv("MP_MIN_C")) minc = atoi(e);
+    if (const char *e = knob("MP_MIN_C")) minc = atoi(e);
     minc = std::min(minc, cmax);
     int64_t minc_cnt = sms * 3 / 8;  // 55 on B200 (50: config 3 128 ms, 55: 123 ms, 64: config 4 +1.4%)
-    if (const char *e = getenv("MP_MIN_C_CNT")) minc_cnt = atoll(e);
+    if (const char *e = knob("MP_MIN_C_CNT")) minc_cnt = atoll(e);
     // Hub instances (h->hub >= 8): the small rounds' longest tiles hold the
     // hub rows and are exact-step bound; 8 bands of few-lane warps (the
     // fewest lanes, whole band columns, with <= 14 compute warps) spread a
     // row's exact steps over more warps.  Measured, config 3 (hub 83):
     // 105.7 -> 95.3 ms/pass (C = 8 with 30 / 20 / 15 lanes: 104.4 / 98.9 /
     // 95.3); config 2 (hub 1.6) would lose 2% with it, so it stays off there.
-    bool hubby = h->hub >= 8.0 && !getenv("MP_NO_HUB");
+    bool hubby = h->hub >= 8.0 && !knob("MP_NO_HUB");
     mp_handle::RoundCfg hub_shape;
     if (hubby) {
         int C = std::min(8, std::min(cmax, b));
-        if (const char *e = getenv("MP_HUB_C")) C = std::max(2, std::min(std::min(cmax, b), atoi(e)));
+        if (const char *e = knob("MP_HUB_C")) C = std::max(2, std::min(std::min(cmax, b), atoi(e)));
         const int RB = (b + C - 1) / C;
         int lw = 32;
         for (int l = RB; l <= 32; l += RB)
@@ -834,7 +913,7 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
                 lw = l;
                 break;
             }
-        if (const char *e = getenv("MP_HUB_LANES")) lw = std::max(1, std::min(32, atoi(e)));
+        if (const char *e = knob("MP_HUB_LANES")) lw = std::max(1, std::min(32, atoi(e)));
         hub_shape = round_shape(h, C, lw);
         hubby = C > 1 && (C - 1) * RB < b && hub_shape.S <= MAX_SLOTS && hub_shape.smem <= 227 * 1024;
         // Bands of balanced exact-step weight instead of RB rows each: the
@@ -847,8 +926,8 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         // uniform 5-row bands 92.4 ms/pass; rmax 6 with 14 / 13 / 12 compute
         // warps 83.3 / 86.4 / 86.1; rmax 7 or 8 (W = 256 then) 97.9 / 97.6)
         int rmax = 6;
-        if (const char *e = getenv("MP_HUB_RMAX")) rmax = atoi(e);
-        if (hubby && rmax > 0 && (int64_t)h->deg.size() > b && !getenv("MP_NO_HUB_SPLIT")) {
+        if (const char *e = knob("MP_HUB_RMAX")) rmax = atoi(e);
+        if (hubby && rmax > 0 && (int64_t)h->deg.size() > b && !knob("MP_NO_HUB_SPLIT")) {
             std::vector<double> w((size_t)b);
             for (int r = 0; r < b; ++r) w[(size_t)r] = std::pow((double)std::max(h->deg[(size_t)r + 1], 1), 1.5);
             const std::vector<int> split = balanced_split(w, C, rmax);
@@ -871,7 +950,7 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         const int64_t cnt = cnt_r[r];
         mp_handle::RoundCfg best = one;
         bool found = false;
-        if (const char *e = getenv("MP_FORCE_C")) {  // experiment: one C for every round, in waves if need be
+        if (const char *e = knob("MP_FORCE_C")) {  // experiment: one C for every round, in waves if need be
             const int C = std::max(1, std::min(MP_CMAX, atoi(e)));
             if (C > 1 && (C - 1) * ((b + C - 1) / C) < b) {
                 if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
@@ -915,7 +994,7 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     // ring block, so the family's barrier depth (~n^2/(2b) levels) shrinks to
     // ~2n (dataflow depth half the barrier depth; all of it here).
     h->df_on = false;
-    if (h->df_allowed && h->kind == MP_SCHEDULE_TILED && !getenv("MP_NO_DF")) {
+    if (h->df_allowed && h->kind == MP_SCHEDULE_TILED && !knob("MP_NO_DF")) {
         size_t r0 = cnt_r.size();
         for (size_t r = 0; r < cnt_r.size(); ++r)
             if (h->round_cnt[r] && h->tile_x[(size_t)h->round_off[r]] >= 1) {
@@ -949,11 +1028,11 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
                 break;
             }
         C = std::min(C, std::min(cmax, b));
-        if (const char *e = getenv("MP_DF_C")) C = std::max(1, std::min(std::min(cmax, b), atoi(e)));
+        if (const char *e = knob("MP_DF_C")) C = std::max(1, std::min(std::min(cmax, b), atoi(e)));
         while (C > 1 && (C - 1) * ((b + C - 1) / C) >= b) --C;
         if (r0 < cnt_r.size() && ndf > 0) {
             int lanes = 0;
-            if (const char *e = getenv("MP_DF_LANES")) lanes = atoi(e);
+            if (const char *e = knob("MP_DF_LANES")) lanes = atoi(e);
             const mp_handle::RoundCfg c = round_shape(h, C, lanes);
             if (c.S <= MAX_SLOTS && c.smem <= 227 * 1024 && max_active_clusters(h, c) >= 1) {
                 for (size_t r = r0; r < cnt_r.size(); ++r) h->rcfg[r] = c;
@@ -1093,8 +1172,8 @@ TileArgs tile_args(mp_handle *h) {
     ta.b = h->b;
     ta.kc = h->kc;
     ta.trace = h->trace;
-    ta.tl_round = getenv("MP_TL_ROUND") ? atoi(getenv("MP_TL_ROUND")) : -1;
-    ta.tl_tile = getenv("MP_TL_TILE") ? atoi(getenv("MP_TL_TILE")) : 0;
+    ta.tl_round = knob("MP_TL_ROUND") ? atoi(knob("MP_TL_ROUND")) : -1;
+    ta.tl_tile = knob("MP_TL_TILE") ? atoi(knob("MP_TL_TILE")) : 0;
     ta.eps = h->eps;
     ta.rp = h->pool[h->rp];
     ta.wp = h->pool[h->rp ^ 1];
@@ -1183,21 +1262,55 @@ int pass_round(mp_handle *h, size_t r, TileArgs &ta) {
 }
 
 bool round_exchanges(const mp_handle *h, size_t r) {
-    return h->sh.on && h->sh.world > 1 && h->round_cnt[r] > 0 && h->sh.round_max[r] > 0;
+    return h->sh.on && h->sh.world > 1 && h->sh.round_any[r];
 }
 
 int pass_pack(mp_handle *h, size_t r) {
-    foot_copy_kernel<true><<<(unsigned)h->round_cnt[r], 256, 0, h->st>>>(
-        h->sh.d_foot + h->round_off[r], h->x, h->ld, h->b, h->sh.sendbuf, 0, h->sh.rank);
+    if (!h->sh.sp_cnt[r]) return MP_OK;
+    piece_copy_kernel<true><<<(unsigned)h->sh.sp_cnt[r], 256, 0, h->st>>>(
+        h->sh.d_send_pc + h->sh.sp_off[r], h->x, h->ld, h->sh.sendbuf);
     CK(cudaGetLastError());
     return MP_OK;
 }
 
 int pass_unpack(mp_handle *h, size_t r) {
-    foot_copy_kernel<false><<<(unsigned)h->round_cnt[r], 256, 0, h->st>>>(
-        h->sh.d_foot + h->round_off[r], h->x, h->ld, h->b, h->sh.recvbuf, h->sh.round_max[r],
-        h->sh.rank);
+    if (!h->sh.rp_cnt[r]) return MP_OK;
+    piece_copy_kernel<false><<<(unsigned)h->sh.rp_cnt[r], 256, 0, h->st>>>(
+        h->sh.d_recv_pc + h->sh.rp_off[r], h->x, h->ld, h->sh.recvbuf);
     CK(cudaGetLastError());
+    return MP_OK;
+}
+
+// After round r: every rank's packed segments to the ranks of the next
+// touchers.  NCCL: one group of point-to-point sends and receives on the
+// session stream; local transport (test harness): device copies.
+int pass_exchange(std::vector<mp_handle *> &hs, size_t r) {
+    mp_handle *h0 = hs[0];
+    const int world = h0->sh.world;
+    if (h0->sh.local) {
+        for (mp_handle *dst : hs)
+            for (mp_handle *src : hs) {
+                const int64_t cnt = src->sh.scnt[r * world + dst->sh.rank];
+                if (src == dst || !cnt) continue;
+                CK(cudaMemcpyAsync(dst->sh.recvbuf + dst->sh.roff[r * world + src->sh.rank],
+                                   src->sh.sendbuf + src->sh.soff[r * world + dst->sh.rank],
+                                   (size_t)cnt * sizeof(double), cudaMemcpyDeviceToDevice, h0->st));
+            }
+        return MP_OK;
+    }
+    const NcclApi &N = nccl_api();
+    const auto &S = h0->sh;
+    NCK(N.groupStart());
+    for (int g = 0; g < world; ++g) {
+        if (g == S.rank) continue;
+        if (S.scnt[r * world + g])
+            NCK(N.send(S.sendbuf + S.soff[r * world + g], (size_t)S.scnt[r * world + g], ncclFloat64, g, S.comm,
+                       h0->st));
+        if (S.rcnt[r * world + g])
+            NCK(N.recv(S.recvbuf + S.roff[r * world + g], (size_t)S.rcnt[r * world + g], ncclFloat64, g, S.comm,
+                       h0->st));
+    }
+    NCK(N.groupEnd());
     return MP_OK;
 }
 
@@ -1264,18 +1377,7 @@ int enqueue_group_pass(std::vector<mp_handle *> &hs, PassCounters **d_ctrs) {
             int rc = pass_pack(h, r);
             if (rc) return rc;
         }
-        const int64_t cnt = h0->sh.round_max[r];
-        if (h0->sh.local) {
-            for (mp_handle *dst : hs)
-                for (mp_handle *src : hs)
-                    if (src != dst)
-                        CK(cudaMemcpyAsync(dst->sh.recvbuf + (int64_t)src->sh.rank * cnt, src->sh.sendbuf,
-                                           (size_t)cnt * sizeof(double), cudaMemcpyDeviceToDevice,
-                                           h0->st));
-        } else {
-            NCK(nccl_api().allGather(h0->sh.sendbuf, h0->sh.recvbuf, (size_t)cnt, ncclFloat64,
-                                     h0->sh.comm, h0->st));
-        }
+        if (int rc = pass_exchange(hs, r)) return rc;
         for (mp_handle *h : hs) {
             int rc = pass_unpack(h, r);
             if (rc) return rc;
@@ -1373,12 +1475,18 @@ extern "C" {
 
 const char *mp_last_error(void) { return g_err.c_str(); }
 
-const char *mp_version(void) { return "metricproj_b200 0.1.0 (sm_100a)"; }
+const char *mp_version(void) {
+#ifdef MP_KNOBS
+    return "metricproj_b200 0.2.0 (sm_100a, +knobs)";
+#else
+    return "metricproj_b200 0.2.0 (sm_100a)";
+#endif
+}
 
 int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     g_err.clear();
     // MP_TIME_CREATE: wall time of the creation phases on stderr
-    const bool tcr = getenv("MP_TIME_CREATE") != nullptr;
+    const bool tcr = knob("MP_TIME_CREATE") != nullptr;
     cudaStream_t tst = nullptr;
     auto tnow = [] {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -1448,7 +1556,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         const bool all_ones = (bits & 0xFFFFFFFFFFFFFull) == 0xFFFFFFFFFFFFFull;
         h->kc.eps = h->eps;
         const bool in_range = h->eps >= 0x1p-60 && h->eps <= 0x1p+60;  // see div_rn
-        h->kc.reps = (all_ones || !in_range || getenv("MP_NO_FASTDIV")) ? 0.0 : 1.0 / h->eps;
+        h->kc.reps = (all_ones || !in_range || knob("MP_NO_FASTDIV")) ? 0.0 : 1.0 / h->eps;
         h->kc.r3 = 1.0 / 3.0;
     }
 
@@ -1569,7 +1677,7 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     if (getenv("MP_VERBOSE"))
         fprintf(stderr, "[mp] make_x_tmap %.3f s\n",
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - tm0).count());
-    h->tma_store = getenv("MP_NO_TMA_STORE") ? 0 : 1;
+    h->tma_store = knob("MP_NO_TMA_STORE") ? 0 : 1;
     tmark("x+tmap");
     TRY(cudaMalloc(&h->tmp, m * sizeof(double)));
     if ((rc = upload_packed(h, &h->d, inst->d_flat))) return bail(rc);
@@ -1605,8 +1713,8 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
     // ---- duals and bookkeeping -------------------------------------------------
     // about one chunk per stream: the first pass writes into most streams
     int32_t cap0 = (int32_t)std::min<int64_t>(std::max<int64_t>(4096, h->nstreams + h->nstreams / 4), 1 << 22);
-    if (const char *e = getenv("MP_POOL_CAP0")) cap0 = std::max(1, atoi(e));  // tests: force overflow
-    if (!getenv("MP_POOL_CAP0")) {
+    if (const char *e = knob("MP_POOL_CAP0")) cap0 = std::max(1, atoi(e));  // tests: force overflow
+    if (!knob("MP_POOL_CAP0")) {
         std::lock_guard<std::mutex> lk(g_hint_mu);
         auto it = g_pool_hint.find({n, b, h->kind, h->nstreams});
         if (it != g_pool_hint.end()) cap0 = std::max(cap0, it->second);
@@ -1639,7 +1747,7 @@ int64_t launches_per_pass(const mp_handle *h) {
     for (size_t r = 0; r < h->round_cnt.size(); ++r) {
         if (h->df_on && r > h->df_r0) continue;  // one dataflow launch for the second family
         c += (h->sh.on ? h->sh.my_cnt[r] : h->round_cnt[r]) ? 1 : 0;
-        if (round_exchanges(h, r)) c += 2;  // pack + unpack
+        if (round_exchanges(h, r)) c += (h->sh.sp_cnt[r] > 0) + (h->sh.rp_cnt[r] > 0);  // pack, unpack
     }
     if (h->kind == MP_SCHEDULE_SERIAL)
         for (int64_t cnt : h->cube_cnt) c += cnt ? 1 : 0;
@@ -2131,6 +2239,156 @@ int mp_nccl_unique_id(void *id) {
     return MP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Re-plan the launch shapes for `cnt_r` tiles per round and renumber the dual
+// streams (tile descriptors and stream heads on the device follow).
+int replan(mp_handle *h, const std::vector<int64_t> &cnt_r) {
+    int rc = plan_rounds(h, cnt_r);
+    if (rc) return rc;
+    CK(cudaMemcpy(h->d_tiles, h->tiles.data(), h->tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+    for (auto &p : h->pool) {  // stream heads for the new numbering
+        cudaFree(p.head);
+        p.head = nullptr;
+        CK(cudaMalloc(&p.head, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
+        CK(cudaMemset(p.head, 0xff, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
+    }
+    return MP_OK;
+}
+
+// The exchange plan of rank `rank` (mp_shard.cuh): for every tile of every
+// round, in schedule order, the blocks of its footprint with the rank of each
+// block's next toucher; runs of blocks with one destination become pieces.
+// Every rank enumerates all tiles, so both ends of a (source, destination)
+// pair lay the pieces out alike.
+struct ExchangePlan {
+    std::vector<PieceDesc> send, recv;
+    std::vector<int64_t> sp_off, sp_cnt, rp_off, rp_cnt, scnt, soff, rcnt, roff;
+    std::vector<char> round_any;
+    std::vector<int64_t> pairs;  // per round x source x destination: pairs sent (no padding)
+    int64_t send_max = 0, recv_max = 0, sent = 0, received = 0;
+};
+
+void plan_exchange(const mp_handle *h, const std::vector<int32_t> &owner, int world, int rank,
+                   ExchangePlan &P) {
+    const int64_t n = h->n, b = h->b, nkb = h->nkb, nib = h->nib;
+    const size_t R = h->round_cnt.size();
+    auto tile_at = [&](int64_t I, int64_t K) -> int32_t {
+        return (I < 0 || K < 0 || I >= nib || K >= nkb) ? -1 : h->tile_of_blk[(size_t)(I * nkb + K)];
+    };
+    auto exists = [&](int64_t I, int64_t K) { return tile_at(I, K) >= 0; };
+    auto row_block = [&](int64_t r) { return r <= 0 ? (int64_t)0 : (r + b - 1) / b; };
+    auto col_block = [&](int64_t c) { return (n - 1 - c) / b; };
+    P.scnt.assign(R * world, 0);
+    P.rcnt.assign(R * world, 0);
+    P.soff.assign(R * world, 0);
+    P.roff.assign(R * world, 0);
+    P.round_any.assign(R, 0);
+    P.pairs.assign(R * world * world, 0);
+    std::vector<std::vector<PieceDesc>> sp((size_t)world), rp((size_t)world);  // this round, per peer
+    std::vector<int64_t> cnt((size_t)world * world);                          // this round, src x dst
+    for (size_t r = 0; r < R; ++r) {
+        for (auto &v : sp) v.clear();
+        for (auto &v : rp) v.clear();
+        std::fill(cnt.begin(), cnt.end(), 0);
+        // rectangle rows [r0, r1] x columns [c0, c1] from `src` to `dst` (-1: every other rank)
+        auto add = [&](int src, int dst, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+            if (r1 < r0 || c1 < c0) return;
+            int64_t valid = 0;  // pairs row < col of the rectangle
+            for (int64_t q = r0; q <= r1; ++q) valid += std::max<int64_t>(0, c1 - std::max(c0, q + 1) + 1);
+            for (int d = 0; d < world; ++d) {
+                if (d == src || (dst >= 0 && d != dst)) continue;
+                P.pairs[(r * world + src) * world + d] += valid;
+                int64_t &off = cnt[(size_t)src * world + d];
+                const int64_t nr = r1 - r0 + 1, nc = c1 - c0 + 1;
+                // split into pieces of at most PIECE_MAX values along the longer side
+                const int64_t rh = nc >= nr ? nr : std::max<int64_t>(1, PIECE_MAX / nc);
+                const int64_t cw = nc >= nr ? std::max<int64_t>(1, PIECE_MAX / nr) : nc;
+                for (int64_t a = 0; a < nr; a += rh)
+                    for (int64_t c = 0; c < nc; c += cw) {
+                        PieceDesc pc;
+                        pc.row0 = (int32_t)(r0 + a);
+                        pc.nrows = (int32_t)std::min(rh, nr - a);
+                        pc.col0 = (int32_t)(c0 + c);
+                        pc.ncols = (int32_t)std::min(cw, nc - c);
+                        pc.off = off;
+                        off += (int64_t)pc.nrows * pc.ncols;
+                        if (src == rank) sp[(size_t)d].push_back(pc);
+                        if (d == rank) rp[(size_t)src].push_back(pc);
+                    }
+            }
+        };
+        for (int64_t t = h->round_off[r]; t < h->round_off[r] + h->round_cnt[r]; ++t) {
+            const TileDesc &T = h->tiles[(size_t)t];
+            const int64_t I = row_block(T.ilo), K = col_block(T.z);
+            const int src = owner[(size_t)t];
+            auto dest = [&](int64_t Ia, int64_t Kb) {  // rank of the block's next toucher, -1: all
+                int64_t nI, nK;
+                if (!next_toucher(Ia, Kb, I, K, exists, nI, nK)) return -1;
+                return (int)owner[(size_t)tile_at(nI, nK)];
+            };
+            add(src, dest(I, K), T.ilo, T.ihi, T.klo, T.z);  // RK
+            // WR: rows R x columns [wr0, wr1], by column block from the lowest columns up
+            const int64_t wr0 = std::max<int64_t>(T.jlo, T.ilo + 1), wr1 = std::min<int64_t>(T.jhi, T.klo - 1);
+            if (wr1 >= wr0) {
+                int cur = -2;
+                int64_t c0 = wr0;
+                for (int64_t kb = col_block(wr0); kb >= col_block(wr1); --kb) {
+                    const int d = dest(I, kb);
+                    const int64_t lo = std::max(wr0, n - b - kb * b);
+                    if (d != cur) {
+                        if (cur != -2) add(src, cur, T.ilo, T.ihi, c0, lo - 1);
+                        cur = d, c0 = lo;
+                    }
+                }
+                add(src, cur, T.ilo, T.ihi, c0, wr1);
+            }
+            // WK: rows [wk0, jhi] x columns K, by row block
+            const int64_t wk0 = std::max<int64_t>(T.jlo, T.ihi + 1);
+            if (T.jhi >= wk0) {
+                int cur = -2;
+                int64_t r0 = wk0;
+                for (int64_t ia = row_block(wk0); ia <= row_block(T.jhi); ++ia) {
+                    const int d = dest(ia, K);
+                    const int64_t lo = std::max<int64_t>(wk0, ia ? 1 + (ia - 1) * b : 0);
+                    if (d != cur) {
+                        if (cur != -2) add(src, cur, r0, lo - 1, T.klo, T.z);
+                        cur = d, r0 = lo;
+                    }
+                }
+                add(src, cur, r0, T.jhi, T.klo, T.z);
+            }
+        }
+        // segments of this rank's buffers, pieces grouped by peer
+        int64_t so = 0, ro = 0;
+        P.sp_off.push_back((int64_t)P.send.size());
+        P.rp_off.push_back((int64_t)P.recv.size());
+        for (int g = 0; g < world; ++g) {
+            P.scnt[r * world + g] = cnt[(size_t)rank * world + g];
+            P.rcnt[r * world + g] = cnt[(size_t)g * world + rank];
+            P.soff[r * world + g] = so;
+            P.roff[r * world + g] = ro;
+            for (PieceDesc pc : sp[(size_t)g]) pc.off += so, P.send.push_back(pc);
+            for (PieceDesc pc : rp[(size_t)g]) pc.off += ro, P.recv.push_back(pc);
+            so += P.scnt[r * world + g];
+            ro += P.rcnt[r * world + g];
+        }
+        P.sp_cnt.push_back((int64_t)P.send.size() - P.sp_off.back());
+        P.rp_cnt.push_back((int64_t)P.recv.size() - P.rp_off.back());
+        P.send_max = std::max(P.send_max, so);
+        P.recv_max = std::max(P.recv_max, ro);
+        P.sent += so;
+        P.received += ro;
+        for (int64_t v : cnt) P.round_any[r] |= v > 0;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
 int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id) {
     g_err.clear();
     if (!h || world < 1 || rank < 0 || rank >= world) return fail(MP_ERR_ARG, "bad argument");
@@ -2140,6 +2398,45 @@ int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id) {
     if (h->pass_index != 0 || h->nnz != 0) return fail(MP_ERR_ARG, "shard a session before its first pass");
     CK(cudaSetDevice(h->dev));
     auto &S = h->sh;
+    // The communicator first: nothing of the session has changed if NCCL is
+    // missing or the rendezvous fails.  (A 1-rank communicator too: it
+    // exercises the same set-up.)
+    ncclComm_t comm = nullptr;
+    if (nccl_id) {
+        const NcclApi &N = nccl_api();
+        if (!N.commInitRank) return fail(MP_ERR_UNSUPPORTED, "NCCL unavailable: %s", N.why.c_str());
+        ncclUniqueId u;
+        std::memcpy(&u, nccl_id, sizeof(u));
+        NCK(N.commInitRank(&comm, world, u, rank));
+    }
+    // Any later failure leaves the session as it was: shard buffers freed, the
+    // communicator destroyed, the unsharded plan (dataflow launch included) back.
+    const bool was_df_allowed = h->df_allowed;
+    bool replanned = false;
+    auto undo = [&](int rc) {
+        const std::string why = g_err;
+        cudaGetLastError();
+        cudaFree(S.d_my_tiles);
+        cudaFree(S.d_send_pc);
+        cudaFree(S.d_recv_pc);
+        cudaFree(S.sendbuf);
+        cudaFree(S.recvbuf);
+        cudaFree(S.d_local);
+        if (S.h_local) cudaFreeHost(S.h_local);
+        if (comm) nccl_api().commDestroy(comm);
+        S = mp_handle::Shard();
+        h->df_allowed = was_df_allowed;
+        if (replanned) replan(h, h->round_cnt);
+        g_err = why;
+        return rc;
+    };
+#define TRY_SHARD(call)                                                                      \
+    do {                                                                                     \
+        const cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                               \
+            return undo(fail(e_ == cudaErrorMemoryAllocation ? MP_ERR_OOM : MP_ERR_CUDA,     \
+                             "mp_shard: %s", cudaGetErrorString(e_)));                       \
+    } while (0)
     std::vector<int64_t> tz;
     for (const TileDesc &t : h->tiles) tz.push_back(t.z);
     lpt_owner(h->b, world, h->tile_x, tz, h->round_cnt, S.owner);
@@ -2157,71 +2454,85 @@ int mp_shard(mp_handle *h, int32_t world, int32_t rank, const void *nccl_id) {
                 per[(size_t)S.owner[(size_t)t]]++;
             share[r] = *std::max_element(per.begin(), per.end());
         }
-        int rc = plan_rounds(h, share);
-        if (rc) return rc;
-        CK(cudaMemcpy(h->d_tiles, h->tiles.data(), h->tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
-        for (auto &p : h->pool) {  // stream heads for the new numbering
-            cudaFree(p.head);
-            p.head = nullptr;
-            CK(cudaMalloc(&p.head, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
-            CK(cudaMemset(p.head, 0xff, (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
-        }
+        replanned = true;
+        if (int rc = replan(h, share)) return undo(rc);
     }
     std::vector<TileDesc> mine;
-    std::vector<FootDesc> foot(h->tiles.size());
-    S.my_off.clear();
-    S.my_cnt.clear();
-    S.round_max.clear();
-    int64_t maxbuf = 0;
     for (size_t r = 0; r < h->round_cnt.size(); ++r) {
-        std::vector<int64_t> used((size_t)world, 0);
         S.my_off.push_back((int64_t)mine.size());
-        int64_t cnt = 0;
-        for (int64_t t = h->round_off[r]; t < h->round_off[r] + h->round_cnt[r]; ++t) {
-            const TileDesc &T = h->tiles[(size_t)t];
-            FootDesc f{};
-            f.t = T;
-            f.wr0 = std::max(T.jlo, T.ilo + 1);
-            f.wrw = std::max(0, std::min(T.jhi, T.klo - 1) - f.wr0 + 1);
-            f.wk0 = std::max(T.jlo, T.ihi + 1);
-            f.nwk = std::max(0, T.jhi - f.wk0 + 1);
-            f.owner = S.owner[(size_t)t];
-            f.off = used[(size_t)f.owner];
-            used[(size_t)f.owner] += foot_count(f, h->b);
-            foot[(size_t)t] = f;
-            if (f.owner == rank) {
-                mine.push_back(T);
-                ++cnt;
-            }
-        }
-        S.my_cnt.push_back(cnt);
-        S.round_max.push_back(*std::max_element(used.begin(), used.end()));
-        maxbuf = std::max(maxbuf, S.round_max.back());
+        for (int64_t t = h->round_off[r]; t < h->round_off[r] + h->round_cnt[r]; ++t)
+            if (S.owner[(size_t)t] == rank) mine.push_back(h->tiles[(size_t)t]);
+        S.my_cnt.push_back((int64_t)mine.size() - S.my_off.back());
     }
-    CK(cudaMalloc(&S.d_my_tiles, std::max<size_t>(mine.size(), 1) * sizeof(TileDesc)));
+    ExchangePlan P;
+    plan_exchange(h, S.owner, world, rank, P);
+    S.sp_off = P.sp_off, S.sp_cnt = P.sp_cnt, S.rp_off = P.rp_off, S.rp_cnt = P.rp_cnt;
+    S.scnt = P.scnt, S.soff = P.soff, S.rcnt = P.rcnt, S.roff = P.roff;
+    S.round_any = P.round_any;
+    S.sent_per_pass = P.sent, S.recv_per_pass = P.received;
+    TRY_SHARD(cudaMalloc(&S.d_my_tiles, std::max<size_t>(mine.size(), 1) * sizeof(TileDesc)));
     if (!mine.empty())
-        CK(cudaMemcpy(S.d_my_tiles, mine.data(), mine.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&S.d_foot, std::max<size_t>(foot.size(), 1) * sizeof(FootDesc)));
-    if (!foot.empty())
-        CK(cudaMemcpy(S.d_foot, foot.data(), foot.size() * sizeof(FootDesc), cudaMemcpyHostToDevice));
+        TRY_SHARD(cudaMemcpy(S.d_my_tiles, mine.data(), mine.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
     if (world > 1) {
-        CK(cudaMalloc(&S.sendbuf, (size_t)std::max<int64_t>(maxbuf, 1) * sizeof(double)));
-        CK(cudaMalloc(&S.recvbuf, (size_t)std::max<int64_t>(maxbuf, 1) * world * sizeof(double)));
+        TRY_SHARD(cudaMalloc(&S.d_send_pc, std::max<size_t>(P.send.size(), 1) * sizeof(PieceDesc)));
+        TRY_SHARD(cudaMalloc(&S.d_recv_pc, std::max<size_t>(P.recv.size(), 1) * sizeof(PieceDesc)));
+        if (!P.send.empty())
+            TRY_SHARD(cudaMemcpy(S.d_send_pc, P.send.data(), P.send.size() * sizeof(PieceDesc), cudaMemcpyHostToDevice));
+        if (!P.recv.empty())
+            TRY_SHARD(cudaMemcpy(S.d_recv_pc, P.recv.data(), P.recv.size() * sizeof(PieceDesc), cudaMemcpyHostToDevice));
+        TRY_SHARD(cudaMalloc(&S.sendbuf, (size_t)std::max<int64_t>(P.send_max, 1) * sizeof(double)));
+        TRY_SHARD(cudaMalloc(&S.recvbuf, (size_t)std::max<int64_t>(P.recv_max, 1) * sizeof(double)));
     }
-    CK(cudaMalloc(&S.d_local, sizeof(PassCounters)));
-    CK(cudaMallocHost(&S.h_local, sizeof(PassCounters)));
+    TRY_SHARD(cudaMalloc(&S.d_local, sizeof(PassCounters)));
+    TRY_SHARD(cudaMallocHost(&S.h_local, sizeof(PassCounters)));
+#undef TRY_SHARD
     std::memset(S.h_local, 0, sizeof(PassCounters));
     S.world = world;
     S.rank = rank;
     S.local = nccl_id == nullptr;
-    if (nccl_id) {  // (a 1-rank communicator too: exercises the same set-up)
-        const NcclApi &N = nccl_api();
-        if (!N.commInitRank) return fail(MP_ERR_UNSUPPORTED, "NCCL unavailable: %s", N.why.c_str());
-        ncclUniqueId u;
-        std::memcpy(&u, nccl_id, sizeof(u));
-        NCK(N.commInitRank(&S.comm, world, u, rank));
-    }
+    S.comm = comm;
     S.on = true;
+    return MP_OK;
+}
+
+int mp_shard_volume(mp_handle *h, int64_t *sent, int64_t *received) {
+    g_err.clear();
+    if (!h || !sent || !received) return fail(MP_ERR_ARG, "bad argument");
+    *sent = h->sh.on ? h->sh.sent_per_pass : 0;
+    *received = h->sh.on ? h->sh.recv_per_pass : 0;
+    return MP_OK;
+}
+
+int mp_shard_route(int64_t n, int32_t b, int32_t world, int64_t *vol, int64_t *nrounds) {
+    g_err.clear();
+    if (n < 3 || b < 1 || world < 1 || !nrounds) return fail(MP_ERR_ARG, "bad argument");
+    mp_handle h;  // host fields only: the schedule
+    h.dev = -1;
+    h.n = n;
+    h.b = b;
+    h.kind = MP_SCHEDULE_TILED;
+    std::vector<int64_t> tz;
+    enumerate_tiles(n, b, h.tile_x, tz, h.round_cnt);
+    *nrounds = (int64_t)h.round_cnt.size();
+    if (!vol) return MP_OK;
+    h.nib = (n + b - 1) / b + 2;
+    h.nkb = (n - 1) / b + 2;
+    h.tile_of_blk.assign((size_t)(h.nib * h.nkb), -1);
+    int64_t off = 0;
+    for (int64_t cnt : h.round_cnt) {
+        h.round_off.push_back(off);
+        off += cnt;
+    }
+    for (size_t t = 0; t < tz.size(); ++t) {
+        const TileDesc T = make_tile(h.tile_x[t], tz[t], b);
+        h.tile_of_blk[(size_t)(((T.ilo + b - 1) / b) * h.nkb + (n - 1 - tz[t]) / b)] = (int32_t)t;
+        h.tiles.push_back(T);
+    }
+    std::vector<int32_t> owner;
+    lpt_owner(b, world, h.tile_x, tz, h.round_cnt, owner);
+    ExchangePlan P;
+    plan_exchange(&h, owner, world, 0, P);
+    std::copy(P.pairs.begin(), P.pairs.end(), vol);
     return MP_OK;
 }
 

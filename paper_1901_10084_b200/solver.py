@@ -176,6 +176,15 @@ class DeviceSession:
             raise NotImplementedError(_native.last_error())
         _native.check(rc, "mp_shard")
 
+    def exchange_volume(self):
+        """(sent, received): 8-byte values this rank moves per pass under the
+        next-toucher exchange plan (mp_shard_volume; 0, 0 when unsharded)."""
+        import ctypes
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(_native.load().mp_shard_volume(self._h, ctypes.byref(a), ctypes.byref(b)),
+                      "mp_shard_volume")
+        return a.value, b.value
+
     def duals_ranked(self):
         """(keys, vals, order): this session's metric duals in visit order and
         the schedule index of each entry's tile (mp_get_duals_ranked)."""

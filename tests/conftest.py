@@ -33,3 +33,14 @@ def oracle_lib():
     from oracle import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture
+def knobs(monkeypatch):
+    """Shape-forcing tests: the experiment switches (MP_CLUSTER, MP_FORCE_C,
+    MP_NO_TMA, MP_POOL_CAP0, ...) exist only in the ``knobs`` library variant
+    (-DMP_KNOBS); the product library ignores them.  Yields the monkeypatch
+    object, with every native call of the test routed to that variant."""
+    from paper_1901_10084_b200 import _native
+    with _native.use_variant(_native.KNOBS_VARIANT):
+        yield monkeypatch

@@ -94,6 +94,65 @@ def test_footprints_cover_touched_pairs_and_are_disjoint(n, b):
             seen |= fp
 
 
+@pytest.mark.parametrize("n,b", [(17, 3), (30, 8), (41, 5), (25, 40), (33, 4), (23, 1), (90, 40)])
+def test_next_toucher_follows_every_pair_through_the_pass(n, b):
+    """A tile's footprint is a union of whole grid blocks, every toucher of a
+    block touches all of its pairs, and the closed-form next toucher is the
+    next tile that touches each pair in schedule order (the last one has
+    none): what the sharded exchange routes by (mp_shard.cuh)."""
+    D = distributed
+    last = {}
+    for rnd in schedule.tiled_rounds(n, b):
+        for t in rnd.units:
+            I, K = D.tile_block(n, b, t)
+            assert D.block_tile(n, b, I, K) == t
+            fp = D.tile_footprint(t, n)
+            union = set()
+            for _, ia, kb in D.footprint_blocks(n, b, I, K):
+                pairs = D.block_pairs(n, b, ia, kb)
+                assert pairs and not (union & pairs)
+                union |= pairs
+                seq = D.block_touchers(n, b, ia, kb)
+                pos = seq.index((I, K))
+                assert D.next_toucher(n, b, ia, kb, I, K) == (seq[pos + 1] if pos + 1 < len(seq) else None)
+            assert union == fp
+            for p in fp:
+                blk = (D.row_block(b, p[0]), D.col_block(n, b, p[1]))
+                if p in last:
+                    assert D.next_toucher(n, b, *blk, *last[p]) == (I, K)
+                else:
+                    assert D.block_touchers(n, b, *blk)[0] == (I, K)
+                last[p] = (I, K)
+    assert len(last) == n * (n - 1) // 2
+    for p, t in last.items():
+        assert D.next_toucher(n, b, D.row_block(b, p[0]), D.col_block(n, b, p[1]), *t) is None
+
+
+@pytest.mark.parametrize("n,b,world", [(60, 8, 2), (100, 40, 4), (200, 16, 8), (45, 6, 3), (23, 1, 2)])
+def test_native_route_matches_python_route(n, b, world):
+    import numpy as np
+    py = np.array(distributed.route_volumes(n, b, world))
+    nat = distributed.native_route_volumes(n, b, world)
+    assert py.shape == nat.shape and np.array_equal(py, nat)
+    assert all(nat[r][g][g] == 0 for r in range(len(nat)) for g in range(world))
+
+
+@pytest.mark.parametrize("n,b,world", [(40, 5, 2), (60, 8, 3), (64, 8, 4)])
+def test_route_volume_is_the_need_plus_one_broadcast(n, b, world):
+    """Without the end-of-pass broadcasts the routed volume is exactly what
+    the ranks need (exchange_volume: pairs whose last writer was another
+    rank); the broadcasts add each pair once per other rank; an all-gather of
+    every footprint would move (world - 1) copies of every touched pair."""
+    import numpy as np
+    need = sum(distributed.exchange_volume(n, b, world))
+    routed = int(np.array(distributed.route_volumes(n, b, world, broadcast=False)).sum())
+    assert routed == need
+    total = int(np.array(distributed.route_volumes(n, b, world)).sum())
+    assert total == need + (world - 1) * (n * (n - 1) // 2)
+    gathered = (world - 1) * schedule.touched_pairs_brute(n, b)
+    assert total < gathered
+
+
 def test_merge_duals_restores_visit_order():
     import numpy as np
     keys = np.arange(10, dtype=np.int64) * 7
@@ -106,12 +165,15 @@ def test_merge_duals_restores_visit_order():
 
 def _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pair_duals, exchange):
     """One pass of rank `rank` of a sharded solve in the reference's arithmetic
-    (oracle.py_pass restated per tile): own tiles only, footprint exchange
-    after every round, pair rows locally (x identical on every rank)."""
+    (oracle.py_pass restated per tile): own tiles only, after every round the
+    blocks of its footprints to the ranks of their next touchers (stale
+    elsewhere until the end-of-pass broadcast), pair rows locally (x identical
+    on every rank by then)."""
     from oracle import oracle as orc
     eps = inst.epsilon
     plan = distributed.shard_rounds(n, b, world)
     rounds = schedule.tiled_rounds(n, b)
+    owner = {distributed.tile_block(n, b, rnd.units[t]): g for rnd, asg in zip(rounds, plan) for t, g in asg}
     new, order, tix = {}, {}, 0
     viol = 0.0
     for rnd, asg in zip(rounds, plan):
@@ -139,9 +201,19 @@ def _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pair_duals, exchange)
                     if theta > 1e-15:
                         new[code + kd] = theta
                         order[code + kd] = tix + t
-        pub = {p: x[orc._pos(n, *p)] for tile in mine for p in distributed.tile_footprint(tile, n)}
+        # every block of this rank's footprints to the rank of its next toucher
+        # (all ranks when this was the block's last toucher of the pass)
+        pub = [dict() for _ in range(world)]
+        for tile in mine:
+            I, K = distributed.tile_block(n, b, tile)
+            for _, ia, kb in distributed.footprint_blocks(n, b, I, K):
+                nxt = distributed.next_toucher(n, b, ia, kb, I, K)
+                dsts = range(world) if nxt is None else [owner[nxt]]
+                for d in dsts:
+                    if d != rank:
+                        pub[d].update({p: x[orc._pos(n, *p)] for p in distributed.block_pairs(n, b, ia, kb)})
         for other in exchange(pub):
-            for p, v in other.items():
+            for p, v in other[rank].items():
                 x[orc._pos(n, *p)] = v
         tix += len(rnd.units)
     viol = max(exchange(viol))

@@ -110,7 +110,7 @@ def test_config5_full_size_sharded_and_resumed():
     _sharded_and_resumed(5, passes=2, world=2)
 
 
-def test_one_cta_tiles_long_rings_deterministic(monkeypatch):
+def test_one_cta_tiles_long_rings_deterministic(knobs):
     """One CTA per tile (MP_CLUSTER=1) at n = 7000: every tile's j-rings wrap
     ~27 times, so a WK slot written back element by element is refilled by a
     TMA box many times per pass.  Regression for a missing producer barrier
@@ -124,9 +124,9 @@ def test_one_cta_tiles_long_rings_deterministic(monkeypatch):
     for env in [{"MP_CLUSTER": "1"}, {"MP_CLUSTER": "1"}, {"MP_CLUSTER": "1", "MP_NO_TMA": "1"},
                 {"MP_FORCE_C": "8"}, {}]:
         for k in ("MP_CLUSTER", "MP_NO_TMA", "MP_FORCE_C"):
-            monkeypatch.delenv(k, raising=False)
+            knobs.delenv(k, raising=False)
         for k, v in env.items():
-            monkeypatch.setenv(k, v)
+            knobs.setenv(k, v)
         s = DeviceSession(inst, "tiled", B)
         s.run(2)
         x, f = s.state()
@@ -136,12 +136,12 @@ def test_one_cta_tiles_long_rings_deterministic(monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"MP_FORCE_C": "8"}, {"MP_FORCE_C": "2"}, {}])
-def test_cluster_waves_bitwise_oracle(oracle_lib, monkeypatch, env):
+def test_cluster_waves_bitwise_oracle(oracle_lib, knobs, env):
     """Clusters in waves (more tiles in a round than the device co-schedules
     as clusters: n = 1400 has rounds of 17 tiles, 8-CTA clusters fit 15 at a
     time) against the oracle, bit for bit, on a Chung-Lu instance (hub rows)."""
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        knobs.setenv(k, v)
     inst = instances.config_instance(3, n=1400)
     sess = DeviceSession(inst, "tiled", B)
     ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=B,

@@ -44,9 +44,9 @@ def test_large_tiles_against_oracle(oracle_lib, config, n, b, passes):
 
 @pytest.mark.parametrize("env", [{"MP_NO_DF": "1"}, {"MP_DF_C": "8"}, {"MP_FORCE_C": "4", "MP_NO_DF": "1"},
                                  {"MP_NO_TMA": "1"}])
-def test_large_tiles_launch_variants(oracle_lib, monkeypatch, env):
+def test_large_tiles_launch_variants(oracle_lib, knobs, env):
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        knobs.setenv(k, v)
     inst = instances.config_instance(2, n=390)
     sess = DeviceSession(inst, "tiled", 64)
     ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=64, workers=4)

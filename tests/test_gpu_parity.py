@@ -210,13 +210,13 @@ def test_fast_division_is_ieee(divisor):
 @pytest.mark.parametrize("cluster,slots", [(1, None), (2, None), (3, None), (5, None), (8, None),
                                            (4, 2), (8, 2), (6, 3)])
 @pytest.mark.parametrize("general_w", [False, True])
-def test_cluster_shapes_bitwise(oracle_lib, monkeypatch, cluster, slots, general_w):
+def test_cluster_shapes_bitwise(oracle_lib, knobs, cluster, slots, general_w):
     """Every launch shape -- C CTAs per tile (row bands, DSMEM forwarding of
     the replicated WK/RK), S slots per thread -- follows the reference order
     bit for bit (MP_CLUSTER caps C; MP_SLOTS raises S)."""
-    monkeypatch.setenv("MP_CLUSTER", str(cluster))
+    knobs.setenv("MP_CLUSTER", str(cluster))
     if slots:
-        monkeypatch.setenv("MP_SLOTS", str(slots))
+        knobs.setenv("MP_SLOTS", str(slots))
     inst = instances.config_instance(1, n=180)
     rx = rf = None
     if general_w:
@@ -241,12 +241,12 @@ def test_cluster_shapes_bitwise(oracle_lib, monkeypatch, cluster, slots, general
 
 
 @pytest.mark.parametrize("kind,cluster", [("tiled", 8), ("tiled", 1), ("serial", 1)])
-def test_dual_pool_overflow_rolls_back(oracle_lib, monkeypatch, kind, cluster):
+def test_dual_pool_overflow_rolls_back(oracle_lib, knobs, kind, cluster):
     """A dual pool far too small: every pass overflows at first, is rolled
     back from its snapshot and redone with a larger pool -- the trajectory
     is unchanged (solver.run_pass semantics, bitwise vs the oracle)."""
-    monkeypatch.setenv("MP_POOL_CAP0", "2")
-    monkeypatch.setenv("MP_CLUSTER", str(cluster))
+    knobs.setenv("MP_POOL_CAP0", "2")
+    knobs.setenv("MP_CLUSTER", str(cluster))
     inst = instances.config_instance(1, n=120)
     sess = DeviceSession(inst, kind, 40)
     ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, kind=kind, b=40)
@@ -266,13 +266,13 @@ def test_dual_pool_overflow_rolls_back(oracle_lib, monkeypatch, kind, cluster):
 @pytest.mark.parametrize("n", [180, 181])  # even n: TMA boxes for WK; odd n: odd klo, element copies
 @pytest.mark.parametrize("cluster", [8, 4, 1])
 @pytest.mark.parametrize("env", [{}, {"MP_WR_PITCH_W": "1", "MP_WK_PITCH_B": "1"}, {"MP_NO_TMA": "1"}])
-def test_ring_staging_variants_bitwise(oracle_lib, monkeypatch, n, cluster, env):
+def test_ring_staging_variants_bitwise(oracle_lib, knobs, n, cluster, env):
     """Every way of staging the j-rings -- WK as 2-D TMA boxes (plain or
     padded row pitch, box or 16-byte write-back) or element by element,
     padded or plain WR pitch -- gives the reference trajectory bit for bit."""
-    monkeypatch.setenv("MP_CLUSTER", str(cluster))
+    knobs.setenv("MP_CLUSTER", str(cluster))
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        knobs.setenv(k, v)
     inst = instances.config_instance(2, n=n)
     sess = DeviceSession(inst, "tiled", 40)
     ref = oracle_lib.OracleSolver(inst.n, inst.d_flat, inst.w_flat, inst.epsilon, b=40, workers=4)

@@ -1,7 +1,9 @@
 """Sharded execution of one instance on the device: every
 rank of a LocalShardGroup runs through the same per-round code as an NCCL
-rank (own tiles, footprint pack / exchange / unpack, counter all-reduce), so
-the group must follow the single-session trajectory bit for bit."""
+rank (own tiles, pack of the footprint blocks for their next touchers' ranks,
+exchange, unpack, counter all-reduce), so the group must follow the
+single-session trajectory bit for bit -- on every rank, although between the
+pair phases a rank's x is current only where it is about to be read."""
 
 import numpy as np
 import pytest
@@ -64,6 +66,30 @@ def test_local_group_matches_oracle(n, b, world, general_w):
     rk, rv = ref.duals()
     assert np.array_equal(np.sort(gk), np.sort(rk))
     grp.close()
+
+
+def test_exchange_volume_follows_the_route_plan():
+    """Each member packs what the host plan routes from it (rectangles: the
+    pairs plus padding at the diagonal), what is sent is received, and the
+    plan moves far less than an all-gather of every footprint."""
+    from paper_1901_10084_b200 import schedule
+    n, b, world = 300, 16, 4
+    inst = instances.config_instance(2, n=n)
+    grp = distributed.LocalShardGroup(inst, world, b)
+    vol = distributed.native_route_volumes(n, b, world)
+    sent = recv = 0
+    for g, s in enumerate(grp.members):
+        sv, rv = s.exchange_volume()
+        assert vol[:, g, :].sum() <= sv <= 1.5 * vol[:, g, :].sum()
+        assert vol[:, :, g].sum() <= rv <= 1.5 * vol[:, :, g].sum()
+        sent += sv
+        recv += rv
+    assert sent == recv
+    assert sent < 0.5 * (world - 1) * schedule.touched_pairs(n, b)
+    grp.close()
+    s = DeviceSession(inst, "tiled", b)
+    assert s.exchange_volume() == (0, 0)
+    s.close()
 
 
 def test_local_group_resumes_from_imported_duals():

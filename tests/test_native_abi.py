@@ -36,6 +36,25 @@ def test_library_builds_and_exports_every_symbol():
     assert b"sm_100a" in L.mp_version()
 
 
+def test_product_library_has_no_experiment_switches():
+    """The launch-shape / timing switches live in the ``knobs`` variant only
+    (-DMP_KNOBS); the product library reads MP_NCCL_LIB and MP_VERBOSE."""
+    prod, knobs = _native.build_all()
+    names = (b"MP_CLUSTER", b"MP_FORCE_C", b"MP_NO_TMA", b"MP_POOL_CAP0", b"MP_MIN_C", b"MP_NO_DF",
+             b"MP_SLOTS", b"MP_HUB_C")
+    blob = open(prod, "rb").read()
+    assert not [n for n in names if n in blob]
+    assert b"MP_NCCL_LIB" in blob and b"MP_VERBOSE" in blob
+    kblob = open(knobs, "rb").read()
+    assert all(n in kblob for n in names)
+    lib = ctypes.CDLL(knobs)
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    with _native.use_variant(_native.KNOBS_VARIANT):
+        assert b"+knobs" in _native.load().mp_version()
+    assert b"+knobs" not in _native.load().mp_version()
+
+
 def test_sass_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", _native.build()], capture_output=True,
