@@ -627,9 +627,14 @@ int smem_optin(const void *k, size_t bytes) {
     return MP_OK;
 }
 
-// One launch per round: ntiles tiles, C CTAs (one cluster) per tile.
+// One launch per round: ntiles tiles, C CTAs (one cluster) per tile.  The
+// kernel's shared-memory opt-in is process-wide state: it is set and the
+// launch issued under one lock, so sessions driven from several host threads
+// (ctypes releases the GIL) cannot change it between the two.
+std::mutex g_launch_mu;
 int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, int ntiles) {
     TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
+    std::lock_guard<std::mutex> launch_lock(g_launch_mu);
     if (int rc = smem_optin((const void *)k, c.smem)) return rc;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = tile_launch_config(c, ntiles, h->st, attr);
@@ -640,6 +645,7 @@ int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, 
 // How many clusters of this shape the device can run at once (0 on error).
 int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
     TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
+    std::lock_guard<std::mutex> launch_lock(g_launch_mu);
     if (smem_optin((const void *)k, c.smem) != MP_OK) return 0;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = tile_launch_config(c, 1, h->st, attr);
@@ -945,6 +951,16 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     std::vector<int> cap(17, -1);  // co-resident clusters per C (queried once)
     std::vector<mp_handle::RoundCfg> shape(17);  // launch shape per C (computed once)
     std::vector<bool> have(17, false);
+    // A shape taken regardless of the round's tile count (waves) must still be
+    // placeable: at least one such cluster fits the device (a MIG slice, an
+    // MPS SM limit or a smaller part may not hold 6 or 8 CTAs of one cluster).
+    auto placeable = [&](int C) {
+        if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
+        if (shape[C].S > MAX_SLOTS || shape[C].smem > 227 * 1024) return false;
+        if (cap[C] < 0) cap[C] = max_active_clusters(h, shape[C]);
+        return cap[C] >= 1;
+    };
+    if (hubby && max_active_clusters(h, hub_shape) < 1) hubby = false;
     h->rcfg.clear();
     for (size_t r = 0; r < cnt_r.size(); ++r) {
         const int64_t cnt = cnt_r[r];
@@ -952,10 +968,7 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         bool found = false;
         if (const char *e = knob("MP_FORCE_C")) {  // experiment: one C for every round, in waves if need be
             const int C = std::max(1, std::min(MP_CMAX, atoi(e)));
-            if (C > 1 && (C - 1) * ((b + C - 1) / C) < b) {
-                if (!have[C]) shape[C] = round_shape(h, C), have[C] = true;
-                if (shape[C].S <= MAX_SLOTS && shape[C].smem <= 227 * 1024) best = shape[C];
-            }
+            if (C > 1 && (C - 1) * ((b + C - 1) / C) < b && placeable(C)) best = shape[C];
             h->rcfg.push_back(best);
             continue;
         }
@@ -975,18 +988,16 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
         // small rounds: at least minc CTAs per tile (see minc above)
         if (hubby && cnt > 0 && cnt <= minc_cnt) {
             best = hub_shape;
-        } else if (best.C < minc && cnt > 0 && cnt <= minc_cnt && (minc - 1) * ((b + minc - 1) / minc) < b) {
-            if (!have[minc]) shape[minc] = round_shape(h, minc), have[minc] = true;
-            if (shape[minc].S <= MAX_SLOTS && shape[minc].smem <= 227 * 1024) best = shape[minc];
+        } else if (best.C < minc && cnt > 0 && cnt <= minc_cnt && (minc - 1) * ((b + minc - 1) / minc) < b &&
+                   placeable(minc)) {
+            best = shape[minc];
         }
         // More tiles than the device co-schedules as clusters: clusters of
         // `fb` CTAs in waves beat one CTA per tile in a single wave (the
         // longest tiles go first and set the round's time; configs 4 / 5:
         // 0.68 -> 0.62 s and 4.8 -> 3.4 s per pass with C = 2 in waves).
-        if (!found && best.C == 1 && cnt > 0 && fb >= 2 && (fb - 1) * ((b + fb - 1) / fb) < b) {
-            if (!have[fb]) shape[fb] = round_shape(h, fb), have[fb] = true;
-            if (shape[fb].S <= MAX_SLOTS && shape[fb].smem <= 227 * 1024) best = shape[fb];
-        }
+        if (!found && best.C == 1 && cnt > 0 && fb >= 2 && (fb - 1) * ((b + fb - 1) / fb) < b && placeable(fb))
+            best = shape[fb];
         h->rcfg.push_back(best);
     }
     // Second family (x >= 1) as one dataflow launch: tiles of one round wait
