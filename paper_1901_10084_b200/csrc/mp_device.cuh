@@ -1207,7 +1207,7 @@ __device__ __forceinline__ bool level_full(int L, uint32_t base0, const unsigned
 #ifndef MP_COLD_INLINE
 #define MP_COLD_INLINE __forceinline__  // inlined: no call, registers allocated with the sweep (-2.7% at config 2)
 #endif
-template <int S, int W, bool UNIT, bool ALIAS>
+template <int S, int W, bool UNIT, bool ALIAS, int U>
 __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned flagged,
                                           const CtaConst *cc, WarpDuals *wd, DualRegs &dr, int warp,
                                           double viol, const SlotGeom<S> G) {
@@ -1291,7 +1291,7 @@ __device__ MP_COLD_INLINE double cold_batch(int L0, int first, int Le, unsigned 
         if (__any_sync(0xffffffffu, moved) && Lc < Le) {
             unsigned f = 0;
 #pragma unroll
-            for (int u = 1; u < MP_BATCH; ++u) {
+            for (int u = 1; u < U; ++u) {
                 const int Lx = Lc + u;
                 if (Lx <= Le) {  // warp-uniform
                     int qa[S], qc[S], qe[S];
@@ -1489,12 +1489,11 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
 // batch.  If some level of the batch needs the exact step, the batch is
 // finished level by level from that level on (later levels re-checked after
 // the update).
-template <int S, int W, bool UNIT, bool ALIAS>
+template <int S, int W, bool UNIT, bool ALIAS, int U>
 __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const SlotGeom<S> &G,
                                       CtaConst &cc, TileSync &ts, WarpDuals *wd, DualRegs &dr, int warp,
                                       int b, int ihi, int klo, double &viol, int &nbatch) {
     if (La > Lb) return;
-    constexpr int U = MP_BATCH;
     constexpr uint32_t PER_LEVEL = (uint32_t)(S * 96);
     const TileDesc &T = cc.T;
     const int lane = threadIdx.x & 31;
@@ -1610,7 +1609,7 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
             __syncwarp();
 #endif
             if (S == 1) {
-                viol = cold_batch<S, W, UNIT, ALIAS>(L, first, Le, wfl, &cc, wd, dr, warp, viol, G);
+                viol = cold_batch<S, W, UNIT, ALIAS, U>(L, first, Le, wfl, &cc, wd, dr, warp, viol, G);
                 if (!ALIAS) {  // the exact steps may have moved this thread's x_ik
 #pragma unroll
                     for (int s = 0; s < S; ++s) xcr[s] = ld_sh(G.pik[s]);
@@ -1981,7 +1980,14 @@ __device__ __noinline__ void ring_producer_tma(unsigned char *sm, const CtaConst
     }
 }
 
-template <int S, int W, bool UNIT>
+// U = levels per batch (one progress publish per batch).  A warp trails its
+// lattice predecessor by a batch, so the chain of warps from a tile's first
+// to its last spans (warps in the chain) x U levels, which -- plus the 2b - 2
+// levels of a warp's own j-window and the blocks loaded ahead -- must fit the
+// ring or the first warps stall on ring slots the last ones still hold: the
+// host picks U = 4 for the 2-CTA shape on the W = 256 ring and MP_BATCH = 8
+// elsewhere (round_shape).
+template <int S, int W, bool UNIT, int U = MP_BATCH>
 __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ CtaConst cc;
@@ -2197,11 +2203,11 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
 #endif
         int nbatch = 0;
         if (mid_a <= mid_b) {
-            sweep<S, W, UNIT, true>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
-            sweep<S, W, UNIT, false>(mid_a, mid_b, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
-            sweep<S, W, UNIT, true>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
+            sweep<S, W, UNIT, true, U>(T.Lbeg, mid_a - 1, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
+            sweep<S, W, UNIT, false, U>(mid_a, mid_b, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
+            sweep<S, W, UNIT, true, U>(mid_b + 1, T.Lend, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
         } else {
-            sweep<S, W, UNIT, true>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
+            sweep<S, W, UNIT, true, U>(T.Lbeg, T.Lend, sm, G, cc, ts, wd, dr, warp, b, ihi, klo, viol, nbatch);
         }
     }
 

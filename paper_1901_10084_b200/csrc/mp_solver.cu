@@ -421,6 +421,7 @@ struct mp_handle {
     // tile, S slots per thread, NWC compute + NPW producer warps per CTA
     struct RoundCfg {
         int C = 1, S = 1, NWC = 1, NPW = 1, NT = 64, W = 128, RB = 1, LW = 32;
+        int U = MP_BATCH;   // levels per batch (progress publish) of a compute warp
         int P = 1;          // WK row pitch in doubles (>= b: see round_shape)
         int PR = 128;       // WR row pitch in doubles (>= W)
         bool colm = false;  // column-major slots in each band
@@ -565,7 +566,10 @@ TileKernel tile_kernel_s(int W, bool unit) {
     return unit ? tile_round_kernel<S, 128, true> : tile_round_kernel<S, 128, false>;
 }
 
-TileKernel tile_kernel_for(int S, int W, bool unit) {
+// U: levels per batch (RoundCfg::U); short batches exist for the shape that
+// needs them (2 slots per thread on the W = 256 ring, see round_shape)
+TileKernel tile_kernel_for(int S, int W, bool unit, int U) {
+    if (U == 4 && S == 2 && W == 256) return tile_round_kernel<2, 256, true, 4>;
     if (W == 512) return S == 1 ? tile_round_kernel<1, 512, true> : tile_round_kernel<2, 512, true>;
     switch (S) {
         case 1: return tile_kernel_s<1>(W, unit);
@@ -633,7 +637,7 @@ int smem_optin(const void *k, size_t bytes) {
 // (ctypes releases the GIL) cannot change it between the two.
 std::mutex g_launch_mu;
 int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, int ntiles) {
-    TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
+    TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x, c.U);
     std::lock_guard<std::mutex> launch_lock(g_launch_mu);
     if (int rc = smem_optin((const void *)k, c.smem)) return rc;
     cudaLaunchAttribute attr[2];
@@ -644,7 +648,7 @@ int launch_tiles(mp_handle *h, const mp_handle::RoundCfg &c, const TileArgs &a, 
 
 // How many clusters of this shape the device can run at once (0 on error).
 int max_active_clusters(const mp_handle *h, const mp_handle::RoundCfg &c) {
-    TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x);
+    TileKernel k = tile_kernel_for(c.S, c.W, h->unit_x, c.U);
     std::lock_guard<std::mutex> launch_lock(g_launch_mu);
     if (smem_optin((const void *)k, c.smem) != MP_OK) return 0;
     cudaLaunchAttribute attr[2];
@@ -813,6 +817,25 @@ mp_handle::RoundCfg round_shape(const mp_handle *h, int C, int lanes = -1,
         // when it at least halves the wavefronts (measured: RB = 5 at b = 40,
         // 5.6 -> 3.3 wavefronts, is a wash; RB >= 8, 8 -> 2, is not)
         if (best * 2.0 <= plain) c.P = bestp;
+    }
+    // Levels per batch: a warp trails its lattice predecessor by one batch, so a
+    // tile's first warp runs (warps on the longest chain) x U levels ahead of
+    // its last, and the ring must hold that plus a warp's own j-window (2b - 2),
+    // the block in use and the blocks loaded ahead -- else the first warps stall
+    // on slots the last ones still hold.  The 2-CTA shape on the W = 256 ring
+    // (chain 2 + 13 warps, S = 2) does not fit with U = 8 (120 + 78 + 80 > 256;
+    // timeline of a config-4 tile: every ~10th batch waits ~14,000 cycles for
+    // the ring, 45% of the sweep) and runs U = 4 (config 4: 506 -> 474 ms/pass;
+    // U = 6: 490; U = 2: 534; more slots per thread instead: 561 / 638).
+    c.U = MP_BATCH;
+    {
+        const int chain = c.colm ? C + c.NWC : C * c.NWC;  // column-major bands: a 2-D grid of warps
+        const int span = chain * MP_BATCH + 2 * b - 2 + BLK * (1 + MP_LOOKAHEAD);
+        if (h->unit_x && c.S == 2 && c.W == 256 && span > c.W) c.U = 4;
+    }
+    if (const char *e = knob("MP_U")) {
+        const int u = atoi(e);
+        if (u == MP_BATCH || (u == 4 && h->unit_x && c.S == 2 && c.W == 256)) c.U = u;
     }
     c.smem = tile_smem_bytes(b, c.W, h->unit_x, c.NWC, c.RB, c.P, c.PR);
     return c;

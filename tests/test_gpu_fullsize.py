@@ -135,11 +135,14 @@ def test_one_cta_tiles_long_rings_deterministic(knobs):
     assert len(hashes) == 1
 
 
-@pytest.mark.parametrize("env", [{"MP_FORCE_C": "8"}, {"MP_FORCE_C": "2"}, {}])
+@pytest.mark.parametrize("env", [{"MP_FORCE_C": "8"}, {"MP_FORCE_C": "2"}, {"MP_FORCE_C": "2", "MP_U": "8"},
+                                 {"MP_DF_C": "2", "MP_U": "8"}, {}])
 def test_cluster_waves_bitwise_oracle(oracle_lib, knobs, env):
     """Clusters in waves (more tiles in a round than the device co-schedules
     as clusters: n = 1400 has rounds of 17 tiles, 8-CTA clusters fit 15 at a
-    time) against the oracle, bit for bit, on a Chung-Lu instance (hub rows)."""
+    time) against the oracle, bit for bit, on a Chung-Lu instance (hub rows).
+    The 2-CTA shape runs batches of 4 levels (its chain of warps does not fit
+    the W = 256 ring with 8, round_shape) -- and batches of 8 with MP_U=8."""
     for k, v in env.items():
         knobs.setenv(k, v)
     inst = instances.config_instance(3, n=1400)
