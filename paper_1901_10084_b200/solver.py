@@ -266,9 +266,32 @@ def _to_stats(s, pass_index):
                      max_violation=s.max_violation, wall_time=s.wall_time, steps=s.steps)
 
 
-def _fill_duals(duals, keys, vals, pd, session):
-    duals.keys = [keys] + [np.empty(0, dtype=np.int64) for _ in range(duals.nworkers - 1)]
-    duals.vals = [vals] + [np.empty(0) for _ in range(duals.nworkers - 1)]
+def worker_of_keys(keys, n, b, p):
+    """Worker that owns each metric dual in a ``workers = p`` reference run:
+    triplet (i, j, k) lies in the tile of row block I = ceil(i / b) and column
+    block K = (n-1-k) // b, which sits at position I (first family, K >= I) or
+    K (second family) of its round and goes to worker (position + 1) mod p
+    (schedule.py:79-80, solver.py:86-91).  ``b = 1`` is the diagonal schedule."""
+    i, _, k, _ = core.decode_keys(keys, n)
+    I = (i + b - 1) // b
+    K = (n - 1 - k) // b
+    return (np.where(K >= I, I, K) + 1) % p
+
+
+def _fill_duals(duals, keys, vals, pd, session, b=None):
+    """Device duals (single-worker visit order) into the store.  With several
+    workers the store gets the reference's per-worker layout (core.py:218-236):
+    a worker's entries are those of its tiles, in visit order -- a stable
+    partition of the single-worker order, since rounds and positions ascend in
+    both."""
+    p = duals.nworkers
+    if p > 1 and b is not None and len(keys):
+        w = worker_of_keys(keys, duals.n, b, p)
+        duals.keys = [keys[w == q] for q in range(p)]
+        duals.vals = [vals[w == q] for q in range(p)]
+    else:
+        duals.keys = [keys] + [np.empty(0, dtype=np.int64) for _ in range(p - 1)]
+        duals.vals = [vals] + [np.empty(0) for _ in range(p - 1)]
     duals.pair_duals = pd
     duals._session = session
     duals._version = session.version
@@ -291,7 +314,7 @@ def run_pass(state, duals, instance, plan, pool=None, pass_index=0):
     state.xv[:] = x
     state.fv[:] = f
     keys, vals, pd = sess.duals()
-    _fill_duals(duals, keys, vals, pd, sess)
+    _fill_duals(duals, keys, vals, pd, sess, None if plan.kind == "serial" else plan.b)
     if err is not None:
         raise SolverError(f"non-finite value in state after pass {pass_index}")
     return _to_stats(st, pass_index)
@@ -343,9 +366,9 @@ def solve(instance, config=None, stats_stream=None):
         if config.fixed_passes is not None and stats:
             converged = _is_converged(stats[-1], config)
         x, f = sess.state()
-        duals = DualStore(instance.n, 1)
+        duals = DualStore(instance.n, config.workers)
         keys, vals, pd = sess.duals()
-        _fill_duals(duals, keys, vals, pd, sess)
+        _fill_duals(duals, keys, vals, pd, sess, None if plan.kind == "serial" else plan.b)
     finally:
         sess.close()
     return Solution(state=PrimalState(instance.n, x, f), stats=stats, converged=converged,

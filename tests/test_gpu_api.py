@@ -236,3 +236,32 @@ def test_dykstra_step_bitwise_reference_golden():
     assert np.array_equal(st3.xv, sg["worked_x"]) and o.theta_plus == float(sg["worked_theta"])
     with pytest.raises(ValueError):
         mp.dykstra_step(st3, core.ConstraintKey(core.Kind.METRIC_IJ, 0, 1, 2), -1.0, inst3)
+
+
+def test_workers_give_the_reference_per_worker_dual_layout():
+    """solve / run_pass with workers = 8: DualStore.keys[w] / vals[w] are the
+    reference's per-worker arrays (core.py:218-236) -- the golden hashes of
+    config 2 were taken over np.concatenate(duals.keys) of the unmodified
+    reference run with 8 workers."""
+    import hashlib
+    from conftest import golden
+    from paper_1901_10084_b200 import solver as S
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    g = golden("config2_n1000_b40_p4")
+    inst = instances.config_instance(2)
+    cfg = S.SolverConfig(workers=8, tile_size=40, schedule_kind="tiled", fixed_passes=int(g["passes"]))
+    plan = S.Plan(inst.n, cfg)
+    state, duals = S.initialize(inst, 8)
+    for k in range(int(g["passes"])):
+        S.run_pass(state, duals, inst, plan, pass_index=k)
+        assert len(duals.keys) == 8
+        keys = np.concatenate(duals.keys) if duals.nnz() else np.empty(0, np.int64)
+        vals = np.concatenate(duals.vals) if duals.nnz() else np.empty(0)
+        assert sha(keys) == g["dkeys_sha"][k] and sha(vals) == g["dvals_sha"][k], k
+        assert sha(state.xv) == g["xsha"][k]
+    sol = S.solve(inst, cfg)
+    assert sha(np.concatenate(sol.duals.keys)) == g["dkeys_sha"][-1]
+    assert sha(np.concatenate(sol.duals.vals)) == g["dvals_sha"][-1]
+    assert sum(len(k_) > 0 for k_ in sol.duals.keys) > 1

@@ -113,3 +113,20 @@ def test_cube_order_equals_serial(n, c):
     assert np.array_equal(states[0][0], states[1][0])
     assert np.array_equal(states[0][1], states[1][1])
     assert states[0][2] == states[1][2]
+
+
+def test_worker_of_keys_matches_round_positions():
+    """The per-worker DualStore layout of a workers = p reference run: a key's
+    worker is (position of its tile in its round + 1) mod p (schedule.py:79-80,
+    solver.py:86-91) -- computed from the key alone."""
+    import numpy as np
+    from paper_1901_10084_b200 import core
+    from paper_1901_10084_b200.solver import worker_of_keys
+    for n, b, p in [(23, 4, 3), (41, 5, 8), (30, 40, 2), (19, 1, 4)]:
+        rounds = schedule.tiled_rounds(n, b) if b > 1 else schedule.diagonal_rounds(n)
+        for rnd in rounds:
+            for pos, unit in enumerate(rnd.units):
+                trips = list(schedule.unit_triplets(unit, n))
+                keys = np.array([core.ConstraintKey(core.Kind.METRIC_IJ, i, j, k).encode(n)
+                                 for (i, j, k) in trips], dtype=np.int64)
+                assert set(worker_of_keys(keys, n, b, p).tolist()) == {rnd.worker_of(pos, p)}
