@@ -278,20 +278,22 @@ def worker_of_keys(keys, n, b, p):
     return (np.where(K >= I, I, K) + 1) % p
 
 
-def _fill_duals(duals, keys, vals, pd, session, b=None):
+def _fill_duals(duals, keys, vals, pd, session, b=None, workers=1):
     """Device duals (single-worker visit order) into the store.  With several
     workers the store gets the reference's per-worker layout (core.py:218-236):
     a worker's entries are those of its tiles, in visit order -- a stable
     partition of the single-worker order, since rounds and positions ascend in
     both."""
-    p = duals.nworkers
+    p = min(workers, duals.nworkers)  # the plan's workers fill the store (solver.py:192-198)
+    rest = duals.nworkers - max(p, 1)
     if p > 1 and b is not None and len(keys):
         w = worker_of_keys(keys, duals.n, b, p)
         duals.keys = [keys[w == q] for q in range(p)]
         duals.vals = [vals[w == q] for q in range(p)]
     else:
-        duals.keys = [keys] + [np.empty(0, dtype=np.int64) for _ in range(p - 1)]
-        duals.vals = [vals] + [np.empty(0) for _ in range(p - 1)]
+        duals.keys, duals.vals, rest = [keys], [vals], duals.nworkers - 1
+    duals.keys += [np.empty(0, dtype=np.int64) for _ in range(rest)]
+    duals.vals += [np.empty(0) for _ in range(rest)]
     duals.pair_duals = pd
     duals._session = session
     duals._version = session.version
@@ -314,7 +316,7 @@ def run_pass(state, duals, instance, plan, pool=None, pass_index=0):
     state.xv[:] = x
     state.fv[:] = f
     keys, vals, pd = sess.duals()
-    _fill_duals(duals, keys, vals, pd, sess, None if plan.kind == "serial" else plan.b)
+    _fill_duals(duals, keys, vals, pd, sess, None if plan.kind == "serial" else plan.b, plan.p)
     if err is not None:
         raise SolverError(f"non-finite value in state after pass {pass_index}")
     return _to_stats(st, pass_index)
@@ -368,7 +370,7 @@ def solve(instance, config=None, stats_stream=None):
         x, f = sess.state()
         duals = DualStore(instance.n, config.workers)
         keys, vals, pd = sess.duals()
-        _fill_duals(duals, keys, vals, pd, sess, None if plan.kind == "serial" else plan.b)
+        _fill_duals(duals, keys, vals, pd, sess, None if plan.kind == "serial" else plan.b, plan.p)
     finally:
         sess.close()
     return Solution(state=PrimalState(instance.n, x, f), stats=stats, converged=converged,
