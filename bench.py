@@ -177,6 +177,20 @@ def ncu_traffic(config, b):
         return None
 
 
+def ncu_counters(config, b):
+    """Pipe / hit-rate counters of the committed full captures (one first-family
+    round and the dataflow launch): FP64 pipe, shared-memory pipe, L2 / L1 hit
+    rates, issue slots; None without a capture for this config."""
+    path = os.path.join(ROOT, "profiles", "ncu_tile_kernel.json")
+    try:
+        with open(path) as fh:
+            e = json.load(fh).get(f"config{config}_b{b}", {})
+        out = {k: e[k] for k in ("first_family_round", "dataflow_launch", "source") if e.get(k)}
+        return out if len(out) > 1 else None
+    except (OSError, ValueError):
+        return None
+
+
 def workload_name(spec, b):
     return (f"config{list_index(spec)}: n={spec.n} {spec.name}, gamma={spec.gamma:g}, "
             f"lambda={spec.lam:g}, tiled b={b}")
@@ -394,6 +408,7 @@ def run_gpu(args):
                 "launches_per_pass": launches / max(args.steps, 1),
                 "barrier_levels_per_pass": schedule.critical_levels(n, b),
                 "ns_per_barrier_level": metric_ms * 1e6 / args.steps / schedule.critical_levels(n, b)}
+    roofline["ncu_counters"] = ncu_counters(args.config, b)
     if args.sharded:  # NVLink exchange of this rank (not part of B_pass)
         roofline["exchange"] = {"scheme": "footprint blocks to the next toucher's rank (grouped send/recv)",
                                 "sent_bytes_per_pass_rank": 8 * xchg[0],

@@ -90,12 +90,35 @@ def full_summary(tag, name="tile"):
     return out
 
 
+def raw_metrics(tag, name="tile"):
+    """FP64-pipe, shared-memory pipe and hit-rate counters of a full capture
+    (`--page raw`): the figures SURVEY 8(d) asks to report beside DRAM GB/s."""
+    rep = os.path.join(OUT, f"prof_{name}_{tag}.ncu-rep")
+    if not os.path.exists(rep):
+        return {}
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return {}
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    want = ("pipe_fp64", "mem_shared", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+            "sm__throughput.avg.pct", "dram__throughput.avg.pct", "smsp__issue_active.avg.pct",
+            "sm__warps_active.avg.pct", "smsp__warps_eligible.avg.per_cycle_active")
+    out = {}
+    for h, u, v in zip(hdr, units, vals):
+        if any(w in h for w in want) and ("pct" in h or "per_cycle" in h or "ratio" in h):
+            out[h] = f"{v} {u}".strip()
+    return out
+
+
 def main(tag, config=3):
     os.makedirs(PROF, exist_ok=True)
     table, per, tot = launches(tag)
     dram = tile_dram(tag)
     full = full_summary(tag)
     full_df = full_summary(tag, "df")
+    raw, raw_df = raw_metrics(tag), raw_metrics(tag, "df")
 
     def stalls(name):
         rep = os.path.join(OUT, f"prof_{name}_{tag}.ncu-rep")
@@ -111,14 +134,20 @@ def main(tag, config=3):
         fh.write(table + "\n\n")
         fh.write(f"## tile_round_kernel, every launch of pass 4 (config {config}, b=40): DRAM bytes\n\n")
         fh.write("```\n" + json.dumps(dram, indent=2) + "\n```\n\n")
-        for title, f, st in (("a first-family round (round 10 of pass 3: hub rows in its longest tile)", full, stall),
-                             ("the dataflow launch of pass 3 (the second family)", full_df, stall_df)):
+        for title, f, st, rw in (("a first-family round (round 10 of pass 3: hub rows in its longest tile)", full, stall, raw),
+                                 ("the dataflow launch of pass 3 (the second family)", full_df, stall_df, raw_df)):
             if not f:
                 continue
             fh.write(f"## Full capture (`--set full`): {title}\n\n```\n")
             for k, v in f.items():
                 fh.write(f"{k:40s} {v}\n")
-            fh.write("```\n\nPer-source-line instruction share and stall samples:\n\n```\n" + st + "```\n\n")
+            fh.write("```\n\n")
+            if rw:
+                fh.write("Pipe and hit-rate counters (`--page raw`):\n\n```\n")
+                for k, v in sorted(rw.items()):
+                    fh.write(f"{k:90s} {v}\n")
+                fh.write("```\n\n")
+            fh.write("Per-source-line instruction share and stall samples:\n\n```\n" + st + "```\n\n")
     path = os.path.join(PROF, "ncu_tile_kernel.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     data[f"config{config}_b40"] = {"dram_bytes_per_pass": dram["dram_bytes_per_pass"],
@@ -126,6 +155,8 @@ def main(tag, config=3):
                                    "dram_bytes_per_launch": dram["dram_bytes_per_launch"],
                                    "l2_bytes_per_launch": dram["l2_bytes_per_launch"],
                                    "launches_measured": dram["launches"],
+                                   "first_family_round": {**{k: full[k] for k in ("L2 Hit Rate", "L1/TEX Hit Rate", "Issue Slots Busy", "Eligible Warps Per Scheduler") if k in full}, **raw},
+                                   "dataflow_launch": {**{k: full_df[k] for k in ("L2 Hit Rate", "L1/TEX Hit Rate", "Issue Slots Busy", "Eligible Warps Per Scheduler") if k in full_df}, **raw_df},
                                    "source": f"{tag}_ncu_summary.md"}
     with open(os.path.join(PROF, "ncu_tile_kernel.json"), "w") as fh:
         json.dump(data, fh, indent=2)
