@@ -102,13 +102,22 @@ def raw_metrics(tag, name="tile"):
     if len(rows) < 3:
         return {}
     hdr, units, vals = rows[0], rows[1], rows[2]
-    want = ("pipe_fp64", "mem_shared", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
-            "sm__throughput.avg.pct", "dram__throughput.avg.pct", "smsp__issue_active.avg.pct",
-            "sm__warps_active.avg.pct", "smsp__warps_eligible.avg.per_cycle_active")
+    want = {"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct_of_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed": "fp64_pipe_pct_of_elapsed",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "shared_pipe_pct_of_elapsed",
+            "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+            "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+            "smsp__warps_eligible.avg.per_cycle_active": "eligible_warps_per_scheduler",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct"}
     out = {}
     for h, u, v in zip(hdr, units, vals):
-        if any(w in h for w in want) and ("pct" in h or "per_cycle" in h or "ratio" in h):
-            out[h] = f"{v} {u}".strip()
+        if h in want:
+            try:
+                out[want[h]] = float(v.replace(",", ""))
+            except ValueError:
+                pass
     return out
 
 
@@ -145,7 +154,7 @@ def main(tag, config=3):
             if rw:
                 fh.write("Pipe and hit-rate counters (`--page raw`):\n\n```\n")
                 for k, v in sorted(rw.items()):
-                    fh.write(f"{k:90s} {v}\n")
+                    fh.write(f"{k:40s} {v:.3f}\n")
                 fh.write("```\n\n")
             fh.write("Per-source-line instruction share and stall samples:\n\n```\n" + st + "```\n\n")
     path = os.path.join(PROF, "ncu_tile_kernel.json")
@@ -155,8 +164,8 @@ def main(tag, config=3):
                                    "dram_bytes_per_launch": dram["dram_bytes_per_launch"],
                                    "l2_bytes_per_launch": dram["l2_bytes_per_launch"],
                                    "launches_measured": dram["launches"],
-                                   "first_family_round": {**{k: full[k] for k in ("L2 Hit Rate", "L1/TEX Hit Rate", "Issue Slots Busy", "Eligible Warps Per Scheduler") if k in full}, **raw},
-                                   "dataflow_launch": {**{k: full_df[k] for k in ("L2 Hit Rate", "L1/TEX Hit Rate", "Issue Slots Busy", "Eligible Warps Per Scheduler") if k in full_df}, **raw_df},
+                                   "first_family_round": raw,
+                                   "dataflow_launch": raw_df,
                                    "source": f"{tag}_ncu_summary.md"}
     with open(os.path.join(PROF, "ncu_tile_kernel.json"), "w") as fh:
         json.dump(data, fh, indent=2)
