@@ -1559,10 +1559,16 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
 #endif
         if (tr) { t1 = clock64(); c_pred += t1 - t0; t0 = t1; }
         const int need = min(Le - jtop0, T.jhi) >> 4;
+#ifdef MP_TIMELINE
+        int tl_spins = 0;
+#endif
 #ifndef MP_EXP_NOWAIT
         while (landed_seen < need) {
             landed_seen = landed_min(ts, C, cc.band);
             if (landed_seen < need) spin_pause();
+#ifdef MP_TIMELINE
+            ++tl_spins;
+#endif
         }
 #endif
         if (tr) { t1 = clock64(); c_ring += t1 - t0; t0 = t1; }
@@ -1640,6 +1646,8 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
             r[1] = (unsigned long long)tl1;
             r[2] = (unsigned long long)clock64();
             r[3] = go_cold ? (S == 1 ? r[3] : 1ull) : 0ull;  // cold_batch wrote 1 | chunk-wait cycles << 8
+            // hot batches: ring polls of this batch and the blocks landed beyond the one needed
+            if (!go_cold) r[3] = ((unsigned long long)tl_spins << 8) | ((unsigned long long)(landed_seen - need) << 32);
         }
 #endif
         ++nbatch;

@@ -42,5 +42,7 @@ def knobs(monkeypatch):
     (-DMP_KNOBS); the product library ignores them.  Yields the monkeypatch
     object, with every native call of the test routed to that variant."""
     from paper_1901_10084_b200 import _native
-    with _native.use_variant(_native.KNOBS_VARIANT):
+    # (a diagnostic variant selected with MP_LIB_VARIANT -- e.g. the checked
+    # build -- has the switches too and stays in place)
+    with _native.use_variant(os.environ.get("MP_LIB_VARIANT") or _native.KNOBS_VARIANT):
         yield monkeypatch

@@ -14,6 +14,7 @@ for n in 150 700; do
   run default $n MP_X=0
   run c1 $n MP_FORCE_C=1 MP_NO_DF=1
   run c2 $n MP_FORCE_C=2 MP_NO_DF=1
+  run c2_u8 $n MP_FORCE_C=2 MP_NO_DF=1 MP_U=8
   run c8 $n MP_FORCE_C=8 MP_NO_DF=1
   run notma_c8 $n MP_FORCE_C=8 MP_NO_TMA=1 MP_NO_DF=1
   run waves $n MP_FORCE_C=2 MP_NO_DF=1 MP_CLUSTER=2
