@@ -1366,7 +1366,7 @@ __device__ __forceinline__ void wait_geq(const int *p, int v, bool sleep) {
     }
 }
 
-struct TileSync {
+struct alignas(16) TileSync {
     unsigned long long wkbar[32];  // per WK ring block slot: its TMA load landed
     int done[32];       // last level each compute warp finished
     int landed_by[16];  // highest ring block landed, per CTA of the cluster
@@ -1444,10 +1444,23 @@ __device__ __forceinline__ int ld_volatile_sh(const int *p) {
     asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
     return v;
 }
-__device__ __forceinline__ int landed_min(TileSync &ts, int C, int band) {
+// Lowest landed block over the cluster's bands: the own band's entry with an
+// acquire (this CTA's warps read that ring), the 16 entries with four vector
+// loads issued together (entries past the cluster size hold 0x3fffffff) -- a
+// loop of scalar volatile loads serialises and cost ~600 cycles per call on
+// the tile's first warp (timeline build, every other ring block).
+__device__ __forceinline__ int landed_min(TileSync &ts, int, int band) {
     int m = ld_acquire(&ts.landed_by[band]);
-    for (int d = 0; d < C; ++d)
-        if (d != band) m = min(m, ld_volatile_sh(&ts.landed_by[d]));
+    const uint32_t a = smem_u32(&ts.landed_by[0]);
+    int v[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        asm volatile("ld.volatile.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[4 * q]), "=r"(v[4 * q + 1]), "=r"(v[4 * q + 2]), "=r"(v[4 * q + 3])
+                     : "r"(a + 16u * q)
+                     : "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) m = min(m, v[q]);
     return m;
 }
 
@@ -2165,7 +2178,9 @@ __global__ void __launch_bounds__(MAX_CTA_THREADS, 1) tile_round_kernel(TileArgs
                                 bk, tid, nt, r0, r1, true);
     }
     cp_async_commit();
-    if (tid < 16) ts.landed_by[tid] = hi0;  // every band lands the same prologue blocks
+    // every band lands the same prologue blocks; entries past the bands with
+    // rows never move and must not bound landed_min
+    if (tid < 16) ts.landed_by[tid] = tid < Ce ? hi0 : 0x3fffffff;
     WarpDuals *wd = wds + (warp < nwc ? warp : 0);
     DualRegs dr;
     if (warp < nwc) rd_init(dr, wd, a.rp, stream_base + warp, lane);
