@@ -1491,7 +1491,11 @@ __device__ __forceinline__ int wait_geq_cluster(uint32_t a, int v) {
         spin_pause();
         x = ld_relaxed_cluster(a);
     }
-    return ld_acquire_cluster(a);
+    // the relaxed load that saw x, then an acquire fence: synchronises with the
+    // release that published x (a second, acquiring load would be another
+    // ~600-cycle round trip through the cluster window)
+    asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+    return x;
 }
 
 
@@ -1594,8 +1598,9 @@ __device__ __forceinline__ void sweep(int La, int Lb, unsigned char *sm, const S
         }
         // progress seen now, for the next batch
         const int lpf = has_loc ? ld_acquire(loc_flag) : 0x3fffffff;
-        // (remote flags are read only when a wait needs them: a remote load
-        // per batch costs more than it saves)
+        // (remote flags are read only when a wait needs them: a relaxed load per
+        // batch issued here, to return under the batch's work, costs more than
+        // it saves -- config 2 4.11 -> 4.22 ms/pass, config 3 81.9 -> 85.4)
         unsigned fl = 0;  // bit u: level L+u has a violated row in some slot of this lane
         if (Le - L + 1 == U) {
             // full batch: straight-line, so the U levels' loads overlap
