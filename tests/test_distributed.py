@@ -163,7 +163,7 @@ def test_merge_duals_restores_visit_order():
     assert k.tolist() == keys.tolist() and v.tolist() == vals.tolist()
 
 
-def _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pair_duals, exchange):
+def _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pair_duals, exchange, p2p):
     """One pass of rank `rank` of a sharded solve in the reference's arithmetic
     (oracle.py_pass restated per tile): own tiles only, after every round the
     blocks of its footprints to the ranks of their next touchers (stale
@@ -201,20 +201,23 @@ def _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pair_duals, exchange)
                     if theta > 1e-15:
                         new[code + kd] = theta
                         order[code + kd] = tix + t
-        # every block of this rank's footprints to the rank of its next toucher
-        # (all ranks when this was the block's last toucher of the pass)
-        pub = [dict() for _ in range(world)]
-        for tile in mine:
-            I, K = distributed.tile_block(n, b, tile)
+        # every block of the round's footprints to the rank of its next toucher
+        # (all ranks when this was the block's last toucher of the pass): both
+        # ends enumerate the round's tiles alike, so a receiver knows how many
+        # values each sender has for it and where they go (mp_shard's plan)
+        route = [[[] for _ in range(world)] for _ in range(world)]  # [src][dst] -> positions
+        for t, g in asg:
+            I, K = distributed.tile_block(n, b, rnd.units[t])
             for _, ia, kb in distributed.footprint_blocks(n, b, I, K):
                 nxt = distributed.next_toucher(n, b, ia, kb, I, K)
-                dsts = range(world) if nxt is None else [owner[nxt]]
-                for d in dsts:
-                    if d != rank:
-                        pub[d].update({p: x[orc._pos(n, *p)] for p in distributed.block_pairs(n, b, ia, kb)})
-        for other in exchange(pub):
-            for p, v in other[rank].items():
-                x[orc._pos(n, *p)] = v
+                for d in (range(world) if nxt is None else [owner[nxt]]):
+                    if d != g:
+                        route[g][d] += [orc._pos(n, *p) for p in sorted(distributed.block_pairs(n, b, ia, kb))]
+        got = p2p([x[route[rank][d]] for d in range(world)],
+                  [len(route[s][rank]) for s in range(world)])
+        for s_ in range(world):
+            if s_ != rank and route[s_][rank]:
+                x[route[s_][rank]] = got[s_]
         tix += len(rnd.units)
     viol = max(exchange(viol))
     return viol, new, order
@@ -232,13 +235,31 @@ def _shard_worker(rank, world, port, q):
         dist.all_gather_object(out, obj)
         return out
 
+    def p2p(send, recv_counts):
+        """Grouped point-to-point exchange (the library's ncclSend / ncclRecv
+        group): send[d] to every other rank d, recv_counts[s] values from s."""
+        import torch
+        ops, bufs = [], [None] * world
+        for d in range(world):
+            if d == rank:
+                continue
+            if len(send[d]):
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(send[d])), d))
+            if recv_counts[d]:
+                bufs[d] = torch.empty(recv_counts[d], dtype=torch.float64)
+                ops.append(dist.P2POp(dist.irecv, bufs[d], d))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return [None if t is None else t.numpy() for t in bufs]
+
     n, b = 14, 3
     inst = instances.random_instance(n, seed=11)
     x = np.zeros(inst.npairs)
     f = -inst.w_flat / inst.epsilon
     duals, pd = {}, np.zeros((inst.npairs, 2))
     for _ in range(3):
-        viol, duals, order = _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pd, exchange)
+        viol, duals, order = _sharded_py_pass(n, b, world, rank, inst, x, f, duals, pd, exchange, p2p)
         # pair rows on every rank (identical x), as in oracle.py_pass
         for p in range(inst.npairs):
             for row in (0, 1):
@@ -261,9 +282,11 @@ def _shard_worker(rank, world, port, q):
 
 
 def test_gloo_sharded_protocol_equals_single_worker_oracle():
-    """Two gloo ranks run the sharded protocol (plan, own tiles, footprint
-    exchange after every round, dual merge); x, f and the merged duals equal
-    the reference-order oracle bit for bit."""
+    """Two gloo ranks run the sharded protocol (plan, own tiles, after every
+    round a grouped point-to-point exchange of the footprint blocks routed to
+    their next touchers -- counts and positions derived on both ends from the
+    plan, as mp_shard does -- dual merge); x, f and the merged duals equal the
+    reference-order oracle bit for bit on both ranks."""
     import numpy as np
     from oracle import oracle as orc
     from paper_1901_10084_b200 import instances
