@@ -922,7 +922,12 @@ int plan_rounds(mp_handle *h, const std::vector<int64_t> &cnt_r) {
     int minc = 6;
     if (const char *e = knob("MP_MIN_C")) minc = atoi(e);
     minc = std::min(minc, cmax);
-    int64_t minc_cnt = sms * 3 / 8;  // 55 on B200 (50: config 3 128 ms, 55: 123 ms, 64: config 4 +1.4%)
+    // Up to 3/8 of the SM count (55 on B200) for uniform instances (config 4:
+    // 40-64 tiles equal, 72: +1%, 90: +4%); up to 2/3 (98) for hub instances,
+    // whose longest tiles are exact-step bound and keep gaining from more CTAs
+    // in larger rounds (config 5: 55 / 72 / 100 / 125 / 150 tiles 3.20 / 3.14 /
+    // 3.06 / 3.06 / 3.13 s per pass; config 3's rounds hold at most 51).
+    int64_t minc_cnt = h->hub >= 8.0 ? sms * 2 / 3 : sms * 3 / 8;
     if (const char *e = knob("MP_MIN_C_CNT")) minc_cnt = atoll(e);
     // Hub instances (h->hub >= 8): the small rounds' longest tiles hold the
     // hub rows and are exact-step bound; 8 bands of few-lane warps (the
