@@ -183,6 +183,16 @@ __global__ void pack_kernel(const double *dense, double *packed, int64_t ld, int
     }
 }
 
+// Pair duals for export: (upper, lower) interleaved as the reference's
+// (npairs, 2) array (core.py:224-228).
+__global__ void interleave2_kernel(const double *a, const double *b, double *out, int64_t m) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        out[2 * p] = a[p];
+        out[2 * p + 1] = b[p];
+    }
+}
+
 // Exact violation scan (_kernels.py:28-57): every metric row of every
 // triplet and both pair rows of every pair.  One CTA per smallest index i
 // (heaviest rows first), warps over j, lanes over k -- x_ik and x_jk are

@@ -27,6 +27,8 @@
 #include <tuple>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <atomic>
 #include <vector>
 
 #include "metricproj_b200.h"
@@ -1599,28 +1601,58 @@ int mp_create(const mp_instance *inst, const mp_config *cfg, mp_handle **out) {
         h->kc.r3 = 1.0 / 3.0;
     }
 
+    // Host scans of the instance (three passes over C(n,2) doubles: 8 ms each at
+    // n = 4000 on one thread) run on all host threads, by ranges of rows.
+    const unsigned scan_threads = m > (1 << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+    auto scan_rows = [&](auto &&body) {  // body(thread, first row, end row)
+        std::vector<std::thread> pool;
+        // rows of equal pair count: row i holds n-1-i pairs, so split the pair range evenly
+        std::vector<int64_t> cut(scan_threads + 1, n);
+        cut[0] = 0;
+        for (unsigned q = 1; q < scan_threads; ++q) {
+            const double frac = (double)q / scan_threads;
+            cut[q] = (int64_t)((double)n * (1.0 - std::sqrt(1.0 - frac)));
+        }
+        for (unsigned q = 1; q < scan_threads; ++q) pool.emplace_back(body, q, cut[q], cut[q + 1]);
+        body(0u, cut[0], cut[1]);
+        for (auto &th : pool) th.join();
+    };
+    auto row_start = [&](int64_t i) { return i * (2 * n - i - 1) / 2; };  // packed index of (i, i+1)
+
     // regularizer checks (core.py:135-140)
-    if (inst->reg_x)
-        for (int64_t p = 0; p < m; ++p) {
-            if (!(inst->reg_x[p] > 0.0)) return bail(fail(MP_ERR_ARG, "regularization weights must be positive"));
-            if (inst->reg_x[p] != 1.0) h->unit_x = false;
-        }
-    if (inst->reg_f)
-        for (int64_t p = 0; p < m; ++p) {
-            if (!(inst->reg_f[p] > 0.0)) return bail(fail(MP_ERR_ARG, "regularization weights must be positive"));
-            if (inst->reg_f[p] != 1.0) h->unit_f = false;
-        }
+    for (int which = 0; which < 2; ++which) {
+        const double *reg = which ? inst->reg_f : inst->reg_x;
+        if (!reg) continue;
+        std::atomic<int> bad{0}, nonunit{0};
+        scan_rows([&](unsigned, int64_t i0, int64_t i1) {
+            int b_ = 0, nu = 0;
+            for (int64_t p = row_start(i0); p < row_start(i1); ++p) {
+                b_ |= !(reg[p] > 0.0);
+                nu |= reg[p] != 1.0;
+            }
+            if (b_) bad = 1;
+            if (nu) nonunit = 1;
+        });
+        if (bad) return bail(fail(MP_ERR_ARG, "regularization weights must be positive"));
+        if (nonunit) (which ? h->unit_f : h->unit_x) = false;
+    }
 
     // ---- hub factor of the instance (plan_rounds) ------------------------------
     if (h->kind != MP_SCHEDULE_SERIAL) {
+        std::vector<std::vector<int32_t>> part(scan_threads, std::vector<int32_t>((size_t)n, 0));
+        scan_rows([&](unsigned q, int64_t i0, int64_t i1) {
+            std::vector<int32_t> &dg = part[q];
+            int64_t p = row_start(i0);
+            for (int64_t i = i0; i < i1; ++i)
+                for (int64_t j = i + 1; j < n; ++j, ++p)
+                    if (inst->d_flat[p] < 0.5) {
+                        ++dg[(size_t)i];
+                        ++dg[(size_t)j];
+                    }
+        });
         std::vector<int32_t> deg((size_t)n, 0);
-        int64_t p = 0;
-        for (int64_t i = 0; i < n; ++i)
-            for (int64_t j = i + 1; j < n; ++j, ++p)
-                if (inst->d_flat[p] < 0.5) {
-                    ++deg[(size_t)i];
-                    ++deg[(size_t)j];
-                }
+        for (const auto &dg : part)
+            for (int64_t i = 0; i < n; ++i) deg[(size_t)i] += dg[(size_t)i];
         int64_t sum = 0;
         int32_t mx = 0;
         for (int32_t v : deg) sum += v, mx = std::max(mx, v);
@@ -1901,23 +1933,18 @@ int mp_get_state(mp_handle *h, double *xv, double *fv) {
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
     const int g = grid_for(h->m, 256, 148 * 16);
-    // through the pinned staging buffer (a pageable copy runs at a fraction
-    // of the link rate)
-    PinnedStage &stage = pinned_stage();
-    std::lock_guard<std::mutex> stage_lock(stage.mu);
+    // Straight into the caller's buffers: the driver stages a pageable copy at
+    // ~18 GB/s on this host, and what dominates either way is the first touch of
+    // the caller's fresh pages; a pinned stage of 2 x 8 m bytes would cost more
+    // to allocate (58 ms per 128 MB) than it ever saves here.
     const size_t mb = (size_t)h->m * sizeof(double);
-    char *stg = static_cast<char *>(stage.get(2 * mb));
     if (xv) {
         pack_kernel<<<g, 256, 0, h->st>>>(h->x, h->tmp, h->ld, h->n, h->m);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(stg ? (void *)stg : (void *)xv, h->tmp, mb, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(xv, h->tmp, mb, cudaMemcpyDeviceToHost, h->st));
     }
-    if (fv) CK(cudaMemcpyAsync(stg ? (void *)(stg + mb) : (void *)fv, h->f, mb, cudaMemcpyDeviceToHost, h->st));
+    if (fv) CK(cudaMemcpyAsync(fv, h->f, mb, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    if (stg) {
-        if (xv) std::memcpy(xv, stg, mb);
-        if (fv) std::memcpy(fv, stg + mb, mb);
-    }
     return MP_OK;
 }
 
@@ -1952,17 +1979,12 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     PinnedStage &stage = pinned_stage();
     std::lock_guard<std::mutex> stage_lock(stage.mu);
     if (pair_duals) {
-        const size_t bytes = 2 * (size_t)h->m * sizeof(double);
-        double *a = static_cast<double *>(stage.get(bytes));
-        if (!a) return fail(MP_ERR_OOM, "pinned staging buffer");
-        double *b = a + h->m;
-        CK(cudaMemcpyAsync(a, h->pu, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaMemcpyAsync(b, h->pl, h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        // interleaved on the device (the pass-start snapshot of x is free between
+        // passes and holds n x ld >= 2 m values), one copy into the caller's array
+        interleave2_kernel<<<grid_for(h->m, 256, 148 * 16), 256, 0, h->st>>>(h->pu, h->pl, h->snap_x, h->m);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(pair_duals, h->snap_x, 2 * (size_t)h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
-        for (int64_t p = 0; p < h->m; ++p) {
-            pair_duals[2 * p] = a[(size_t)p];
-            pair_duals[2 * p + 1] = b[(size_t)p];
-        }
     }
     if (!keys && !vals) return MP_OK;
     const DualPool &P = h->pool[h->rp];
@@ -1985,7 +2007,6 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
         int64_t key;
         double val;
     };
-    std::vector<E> ents;
     if (h->kind == MP_SCHEDULE_SERIAL) {
         // serial visit order is lexicographic (i, j, k, kind) = ascending key code
         std::vector<std::pair<int64_t, double>> all;
@@ -2019,12 +2040,55 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
         }
         return MP_OK;
     }
-    for (size_t t = 0; t < h->tiles.size(); ++t) {
-        ents.clear();
-        const int64_t tx = h->tile_x[t];
+    // Tiles are independent: count each tile's entries (walk its streams'
+    // chunk chains), prefix-sum the counts into output offsets, then decode,
+    // order and write the tiles on all host threads.
+    const size_t nt = h->tiles.size();
+    auto tile_streams = [&](size_t t) {
         const mp_handle::RoundCfg &rc = h->rcfg[(size_t)h->tile_round[t]];
-        for (int w = 0; w < rc.C * rc.NWC; ++w) {
+        return rc.C * rc.NWC;
+    };
+    std::vector<int64_t> toff(nt + 1, 0);
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const unsigned nthreads = used > 4096 ? hw : 1u;
+    auto parallel_tiles = [&](auto &&body) {
+        std::atomic<size_t> next{0};
+        auto work = [&] {
+            for (;;) {
+                const size_t t0 = next.fetch_add(64);
+                if (t0 >= nt) break;
+                for (size_t t = t0; t < std::min(nt, t0 + 64); ++t) body(t);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned q = 1; q < nthreads; ++q) pool.emplace_back(work);
+        work();
+        for (auto &th : pool) th.join();
+    };
+    parallel_tiles([&](size_t t) {
+        int64_t cnt = 0;
+        for (int w = 0; w < tile_streams(t); ++w) {
             int32_t c = used ? hh[(size_t)(h->tiles[t].stream0 + w)] : -1;
+            while (c >= 0 && c < used) {
+                int e = 0;
+                while (e < CHUNK && hr[(size_t)c].keys[e] != KEY_END) ++e;
+                cnt += e;
+                c = hr[(size_t)c].next;
+            }
+        }
+        toff[t + 1] = cnt;
+    });
+    for (size_t t = 0; t < nt; ++t) toff[t + 1] += toff[t];
+    outpos = toff[nt];
+    if (outpos != h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent: %lld vs %lld",
+                                      (long long)outpos, (long long)h->nnz);
+    parallel_tiles([&](size_t t) {
+        if (toff[t + 1] == toff[t]) return;
+        std::vector<E> te;
+        te.reserve((size_t)(toff[t + 1] - toff[t]));
+        const int64_t tx = h->tile_x[t];
+        for (int w = 0; w < tile_streams(t); ++w) {
+            int32_t c = hh[(size_t)(h->tiles[t].stream0 + w)];
             while (c >= 0 && c < used) {
                 for (int e = 0; e < CHUNK; ++e) {
                     const uint32_t key = hr[(size_t)c].keys[e];
@@ -2039,22 +2103,22 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
                     en.rank[4] = dd.kind;
                     en.key = ((dd.i * n + dd.j) * n + dd.k) * 3 + dd.kind;
                     en.val = hr[(size_t)c].vals[e];
-                    ents.push_back(en);
+                    te.push_back(en);
                 }
                 c = hr[(size_t)c].next;
             }
         }
-        std::sort(ents.begin(), ents.end(), [](const E &a, const E &b) {
+        std::sort(te.begin(), te.end(), [](const E &a, const E &b) {
             return std::lexicographical_compare(a.rank, a.rank + 5, b.rank, b.rank + 5);
         });
-        for (const E &en : ents) {
-            if (outpos >= h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent (count)");
-            if (keys) keys[outpos] = en.key;
-            if (vals) vals[outpos] = en.val;
-            if (order) order[outpos] = (int64_t)t;
-            ++outpos;
+        int64_t o = toff[t];
+        for (const E &en : te) {
+            if (keys) keys[o] = en.key;
+            if (vals) vals[o] = en.val;
+            if (order) order[o] = (int64_t)t;
+            ++o;
         }
-    }
+    });
     if (outpos != h->nnz) return fail(MP_ERR_CUDA, "dual store inconsistent: %lld vs %lld",
                                       (long long)outpos, (long long)h->nnz);
     return MP_OK;
