@@ -162,6 +162,25 @@ void pin_release(void *p) {
     if (g_pin_free.size() < 256) g_pin_free.push_back(p);
     else cudaFreeHost(p);
 }
+// First touch of a large output buffer on all host threads: a fresh numpy
+// array costs ~28 ms of page faults per 64 MB when the driver's copy thread
+// takes them one by one (measured on the GPU host); touching one byte per page
+// from 16 threads beforehand takes a few ms.  The buffers are outputs, about to
+// be overwritten.
+void prefault_output(void *p, size_t bytes) {
+    if (!p || bytes < (size_t(8) << 20)) return;
+    const unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    char *base = static_cast<char *>(p);
+    std::vector<std::thread> pool;
+    auto work = [&](unsigned q) {
+        const size_t lo = bytes / nthreads * q, hi = q + 1 == nthreads ? bytes : bytes / nthreads * (q + 1);
+        for (size_t o = lo; o < hi; o += 4096) base[o] = 0;
+    };
+    for (unsigned q = 1; q < nthreads; ++q) pool.emplace_back(work, q);
+    work(0);
+    for (auto &th : pool) th.join();
+}
+
 // Pinned staging for the large device -> host reads (dual pools, pair duals):
 // one process-wide buffer, grown on demand, held under its mutex while used.
 struct PinnedStage {
@@ -1941,8 +1960,10 @@ int mp_get_state(mp_handle *h, double *xv, double *fv) {
     if (xv) {
         pack_kernel<<<g, 256, 0, h->st>>>(h->x, h->tmp, h->ld, h->n, h->m);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(xv, h->tmp, mb, cudaMemcpyDeviceToHost, h->st));
     }
+    prefault_output(xv, mb);  // (under the pack kernel)
+    prefault_output(fv, mb);
+    if (xv) CK(cudaMemcpyAsync(xv, h->tmp, mb, cudaMemcpyDeviceToHost, h->st));
     if (fv) CK(cudaMemcpyAsync(fv, h->f, mb, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     return MP_OK;
@@ -1983,6 +2004,7 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
         // passes and holds n x ld >= 2 m values), one copy into the caller's array
         interleave2_kernel<<<grid_for(h->m, 256, 148 * 16), 256, 0, h->st>>>(h->pu, h->pl, h->snap_x, h->m);
         CK(cudaGetLastError());
+        prefault_output(pair_duals, 2 * (size_t)h->m * sizeof(double));
         CK(cudaMemcpyAsync(pair_duals, h->snap_x, 2 * (size_t)h->m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
     }
