@@ -24,6 +24,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <new>
 #include <tuple>
 #include <mutex>
 #include <string>
@@ -181,31 +183,6 @@ void prefault_output(void *p, size_t bytes) {
     for (auto &th : pool) th.join();
 }
 
-// Pinned staging for the large device -> host reads (dual pools, pair duals):
-// one process-wide buffer, grown on demand, held under its mutex while used.
-struct PinnedStage {
-    std::mutex mu;
-    void *p = nullptr;
-    size_t cap = 0;
-    void *get(size_t sz) {  // caller holds mu
-        if (sz > cap) {
-            if (p) cudaFreeHost(p);
-            p = nullptr;
-            cap = 0;
-            if (cudaMallocHost(&p, sz) != cudaSuccess) {
-                cudaGetLastError();
-                p = nullptr;
-                return nullptr;
-            }
-            cap = sz;
-        }
-        return p;
-    }
-};
-PinnedStage &pinned_stage() {
-    static PinnedStage *s = new PinnedStage();
-    return *s;
-}
 // Dual-pool capacity a previous session of the same shape grew to: the next
 // one starts there (no re-allocation during its first passes, and its pool
 // buffers come back from the cache).
@@ -1997,8 +1974,6 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     g_err.clear();
     if (!h) return fail(MP_ERR_ARG, "null handle");
     CK(cudaSetDevice(h->dev));
-    PinnedStage &stage = pinned_stage();
-    std::lock_guard<std::mutex> stage_lock(stage.mu);
     if (pair_duals) {
         // interleaved on the device (the pass-start snapshot of x is free between
         // passes and holds n x ld >= 2 m values), one copy into the caller's array
@@ -2012,8 +1987,13 @@ int get_duals_impl(mp_handle *h, int64_t *keys, double *vals, double *pair_duals
     const DualPool &P = h->pool[h->rp];
     const int64_t used = h->pool_used[h->rp];
     const size_t rec_bytes = (size_t)used * sizeof(ChunkRec);
-    char *stg = static_cast<char *>(stage.get(rec_bytes + (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t)));
-    if (!stg) return fail(MP_ERR_OOM, "pinned staging buffer");
+    // (pageable: pinning a stage of this size costs more than the copy's ~18
+    // GB/s loses against a pinned one, and the first call of a process pays it)
+    const size_t stg_bytes = rec_bytes + (size_t)std::max<int64_t>(h->nstreams, 1) * sizeof(int32_t);
+    std::unique_ptr<char[]> stg_own(new (std::nothrow) char[stg_bytes]);
+    char *stg = stg_own.get();
+    if (!stg) return fail(MP_ERR_OOM, "dual export buffer");
+    prefault_output(stg, stg_bytes);
     const ChunkRec *hr = reinterpret_cast<const ChunkRec *>(stg);
     const int32_t *hh = reinterpret_cast<const int32_t *>(stg + rec_bytes);
     if (used)
